@@ -1,0 +1,282 @@
+// Auxiliary kernels of the hot path (mode-independent, compiled -fmad=false):
+//   * ghost fill on padded buffers (grid.py:147-175 fill_axis / fill_boundary)
+//   * halo slab pack/unpack for the NCCL exchange (parallel.py:185-254)
+//   * per-sample Welford/Chan moment merge (uq.py:114-158)
+//   * structure-function sums (uq.py:231-273), deterministic two-pass reduce
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/fvb200.h"
+
+namespace fvb {
+
+namespace {
+
+struct Pad {
+  int64_t P[3];   // padded extents (x first); unused axes 1
+  int64_t n[3];   // interior extents
+  int g;
+  int dim;
+};
+
+__host__ __device__ inline Pad make_pad(const fvb_scheme& s) {
+  Pad p;
+  p.g = s.ghost;
+  p.dim = s.dim;
+  for (int k = 0; k < 3; ++k) {
+    p.n[k] = k < s.dim ? s.cells[k] : 1;
+    p.P[k] = k < s.dim ? s.cells[k] + 2 * s.ghost : 1;
+  }
+  return p;
+}
+
+// padded coordinate -> element offset relative to the interior origin
+__device__ inline int64_t poff(const Pad& p, const fvb_layout& L, int64_t px, int64_t py, int64_t pz) {
+  int64_t o = px - (p.dim >= 1 ? p.g : 0);
+  if (p.dim >= 2) o += (py - p.g) * L.sy;
+  if (p.dim >= 3) o += (pz - p.g) * L.sz;
+  return o;
+}
+
+// fill_axis: both ghost slabs of one axis, full padded extent of the others
+__global__ void fill_axis_kernel(Pad p, fvb_layout L, double* u, int ncomp, int ninst, int axis, int periodic) {
+  int64_t E[3] = {p.P[0], p.P[1], p.P[2]};
+  E[axis] = 2 * p.g;
+  const int64_t per = E[0] * E[1] * E[2];
+  const int64_t total = per * ncomp * ninst;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i;
+    int64_t c3[3];
+    c3[0] = r % E[0]; r /= E[0];
+    c3[1] = r % E[1]; r /= E[1];
+    c3[2] = r % E[2]; r /= E[2];
+    const int c = (int)(r % ncomp);
+    const int inst = (int)(r / ncomp);
+    const int64_t j = c3[axis];
+    const int64_t n = p.n[axis];
+    int64_t dst, src;
+    if (j < p.g) {               // low ghosts [0, g)
+      dst = j;
+      src = periodic ? n + j : p.g;
+    } else {                     // high ghosts [n+g, n+2g)
+      dst = n + j;
+      src = periodic ? j : n + p.g - 1;
+    }
+    int64_t d3[3] = {c3[0], c3[1], c3[2]};
+    int64_t s3[3] = {c3[0], c3[1], c3[2]};
+    d3[axis] = dst;
+    s3[axis] = src;
+    double* b = u + L.origin + inst * L.si + c * L.sc;
+    b[poff(p, L, d3[0], d3[1], d3[2])] = b[poff(p, L, s3[0], s3[1], s3[2])];
+  }
+}
+
+// halo slab: side 0 = low face, side 1 = high face.
+// pack reads the g interior layers next to the face, unpack writes the ghosts.
+__global__ void halo_kernel(Pad p, fvb_layout L, double* u, int ncomp, int axis, int side, double* buf,
+                            int unpack) {
+  int64_t E[3] = {p.P[0], p.P[1], p.P[2]};
+  E[axis] = p.g;
+  const int64_t total = E[0] * E[1] * E[2] * ncomp;
+  const int64_t n = p.n[axis];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i;
+    int64_t c3[3];
+    c3[0] = r % E[0]; r /= E[0];
+    c3[1] = r % E[1]; r /= E[1];
+    c3[2] = r % E[2]; r /= E[2];
+    const int c = (int)r;
+    const int64_t j = c3[axis];
+    int64_t a;
+    if (unpack) a = side == 0 ? j : n + p.g + j;  // ghosts
+    else a = side == 0 ? p.g + j : n + j;         // parallel.py:237-239
+    c3[axis] = a;
+    double* b = u + L.origin + c * L.sc;
+    const int64_t o = poff(p, L, c3[0], c3[1], c3[2]);
+    if (unpack) b[o] = buf[i];
+    else buf[i] = b[o];
+  }
+}
+
+// One sample merged into (mean, m2) holding `count` samples.  The sample is
+// a fresh MomentAccumulator after update(v) (uq.py:125-133 with count 0):
+//   om = 0 + (v - 0)/1,  om2 = 0 + (v - 0)*(v - om)
+// merged by uq.py:135-148 (first merge copies).
+__global__ void moments_push_kernel(Pad p, fvb_layout L, const double* u, int ncomp, int inst, double* mean,
+                                    double* m2, long long count) {
+  const int64_t ncell = p.n[0] * p.n[1] * p.n[2];
+  const int64_t total = ncell * ncomp;
+  const double frac = 1.0 / (double)(count + 1);   // other.count / total (int / int)
+  const double fc = (double)count;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i / ncell);
+    int64_t r = i % ncell;
+    const int64_t x = r % p.n[0];
+    r /= p.n[0];
+    const int64_t y = r % p.n[1];
+    const int64_t z = r / p.n[1];
+    const double v = u[L.origin + inst * L.si + c * L.sc + x + y * L.sy + z * L.sz];
+    const double d0 = v - 0.0;
+    const double om = 0.0 + d0 / 1.0;
+    const double om2 = 0.0 + d0 * (v - om);
+    if (count == 0) {
+      mean[i] = om;
+      m2[i] = om2;
+    } else {
+      const double mu = mean[i];
+      const double delta = om - mu;
+      mean[i] = mu + delta * frac;
+      m2[i] = (m2[i] + om2) + ((delta * delta) * fc) * frac;
+    }
+  }
+}
+
+__global__ void moments_merge_kernel(double* ma, double* m2a, long long ca, const double* mb, const double* m2b,
+                                     long long cb, int64_t n) {
+  const double total = (double)(ca + cb);
+  const double frac = (double)cb / total;
+  const double fca = (double)ca;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (cb == 0) continue;
+    if (ca == 0) {
+      ma[i] = mb[i];
+      m2a[i] = m2b[i];
+      continue;
+    }
+    const double delta = mb[i] - ma[i];
+    const double m = ma[i] + delta * frac;
+    m2a[i] = (m2a[i] + m2b[i]) + ((delta * delta) * fca) * frac;
+    ma[i] = m;
+  }
+}
+
+constexpr int kSfThreads = 256;
+
+// Pass 1: per-block partial sums S[h][j] of |w(x + h e_j) - w(x)|^p, where
+// j is the NUMPY axis (0 = slowest), matching np.roll(w, -h, axis=j).
+__global__ void __launch_bounds__(kSfThreads) structure_pass1(Pad p, fvb_layout L, const double* u, int inst,
+                                                              int comp, double pw, int H, double* partials) {
+  __shared__ double red[kSfThreads / 32];
+  const int dim = p.dim;
+  const int64_t ncell = p.n[0] * p.n[1] * p.n[2];
+  const double* w = u + L.origin + inst * L.si + comp * L.sc;
+  for (int h = 0; h <= H; ++h) {
+    for (int j = 0; j < dim; ++j) {
+      const int k = dim - 1 - j;  // spatial axis of numpy axis j
+      double acc = 0.0;
+      for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncell;
+           i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t c3[3];
+        int64_t r = i;
+        c3[0] = r % p.n[0]; r /= p.n[0];
+        c3[1] = r % p.n[1];
+        c3[2] = r / p.n[1];
+        const int64_t o = c3[0] + c3[1] * L.sy + c3[2] * L.sz;
+        int64_t s3[3] = {c3[0], c3[1], c3[2]};
+        s3[k] = (c3[k] + h) % p.n[k];
+        const int64_t os = s3[0] + s3[1] * L.sy + s3[2] * L.sz;
+        const double d = fabs(w[os] - w[o]);
+        acc += pw == 2.0 ? d * d : (pw == 1.0 ? d : pow(d, pw));
+      }
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int q = 0; q < kSfThreads / 32; ++q) s += red[q];
+        partials[((int64_t)blockIdx.x * (H + 1) + h) * dim + j] = s;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Pass 2 (one block): fixed-order sum of the partials, then the reference's
+// accumulation  acc = sum_j mean_j ; sums[h] += acc / dim  (uq.py:257-261).
+__global__ void structure_pass2(const double* __restrict__ partials, int nblocks, int H, int dim, double ncell, double* sums) {
+  __shared__ double red[kSfThreads];
+  __shared__ double S[64 * 3];
+  for (int hj = 0; hj < (H + 1) * dim; ++hj) {
+    double acc = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) acc += partials[(int64_t)b * (H + 1) * dim + hj];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+      if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) S[hj] = red[0];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    for (int h = 0; h <= H; ++h) {
+      double acc = 0.0;
+      for (int j = 0; j < dim; ++j) acc += S[h * dim + j] / ncell;
+      sums[h] += acc / dim;
+    }
+  }
+}
+
+int grid_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace
+
+int launch_fill_axis(const fvb_scheme& s, const fvb_layout& L, double* u, int ninst, int axis, cudaStream_t st) {
+  const Pad p = make_pad(s);
+  int64_t n = (int64_t)2 * p.g * s.ncomp * ninst;
+  for (int k = 0; k < 3; ++k)
+    if (k != axis) n *= p.P[k];
+  fill_axis_kernel<<<grid_for(n), 256, 0, st>>>(p, L, u, s.ncomp, ninst, axis, s.bc[axis] == FVB_BC_PERIODIC);
+  return 0;
+}
+
+int64_t halo_count(const fvb_scheme& s, int axis) {
+  const Pad p = make_pad(s);
+  int64_t n = (int64_t)p.g * s.ncomp;
+  for (int k = 0; k < 3; ++k)
+    if (k != axis) n *= p.P[k];
+  return n;
+}
+
+int launch_halo(const fvb_scheme& s, const fvb_layout& L, double* u, int axis, int side, double* buf, int unpack,
+                cudaStream_t st) {
+  const Pad p = make_pad(s);
+  halo_kernel<<<grid_for(halo_count(s, axis)), 256, 0, st>>>(p, L, u, s.ncomp, axis, side, buf, unpack);
+  return 0;
+}
+
+int launch_moments_push(const fvb_scheme& s, const fvb_layout& L, const double* u, int inst, double* mean,
+                        double* m2, int64_t count_before, cudaStream_t st) {
+  const Pad p = make_pad(s);
+  const int64_t n = p.n[0] * p.n[1] * p.n[2] * s.ncomp;
+  moments_push_kernel<<<grid_for(n), 256, 0, st>>>(p, L, u, s.ncomp, inst, mean, m2, (long long)count_before);
+  return 0;
+}
+
+int launch_moments_merge(double* ma, double* m2a, int64_t ca, const double* mb, const double* m2b, int64_t cb,
+                         int64_t n, cudaStream_t st) {
+  moments_merge_kernel<<<grid_for(n), 256, 0, st>>>(ma, m2a, (long long)ca, mb, m2b, (long long)cb, n);
+  return 0;
+}
+
+int structure_blocks(const fvb_scheme& s) {
+  const Pad p = make_pad(s);
+  return grid_for(p.n[0] * p.n[1] * p.n[2]) > 148 * 4 ? 148 * 4 : grid_for(p.n[0] * p.n[1] * p.n[2]);
+}
+
+int launch_structure(const fvb_scheme& s, const fvb_layout& L, const double* u, int inst, int comp, double pw,
+                     int H, double* d_sums, double* d_partials, int nblocks, cudaStream_t st) {
+  const Pad p = make_pad(s);
+  structure_pass1<<<nblocks, kSfThreads, 0, st>>>(p, L, u, inst, comp, pw, H, d_partials);
+  structure_pass2<<<1, kSfThreads, 0, st>>>(d_partials, nblocks, H, s.dim, (double)(p.n[0] * p.n[1] * p.n[2]),
+                                            d_sums);
+  return 0;
+}
+
+}  // namespace fvb

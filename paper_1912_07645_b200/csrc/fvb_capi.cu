@@ -1,0 +1,713 @@
+// C ABI of the B200 finite-volume hot path (include/fvb200.h).
+//
+// Owns: the context (device, stream, scratch, error text), the
+// device-resident run loop (CUDA-graph batches of whole SSP-RK steps with dt,
+// t and the stop flag kept in device memory), and the dispatch into the two
+// compiled arithmetic modes (namespace exact: bitwise == reference; fast).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/fvb200.h"
+#include "fvb_state.cuh"
+
+namespace fvb {
+namespace exact {
+int launch_stage(int dim, int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s);
+int launch_speed(int dim, int eq, const StageParams& p, int finalize, dim3 grid, cudaStream_t s);
+void stage_block(int dim, int& nt, int& nty);
+}  // namespace exact
+namespace fast {
+int launch_stage(int dim, int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s);
+int launch_speed(int dim, int eq, const StageParams& p, int finalize, dim3 grid, cudaStream_t s);
+void stage_block(int dim, int& nt, int& nty);
+}  // namespace fast
+// fvb_aux.cu
+int launch_fill_axis(const fvb_scheme& s, const fvb_layout& L, double* u, int ninst, int axis, cudaStream_t st);
+int launch_halo(const fvb_scheme& s, const fvb_layout& L, double* u, int axis, int side, double* buf,
+                int unpack, cudaStream_t st);
+int64_t halo_count(const fvb_scheme& s, int axis);
+int launch_moments_push(const fvb_scheme& s, const fvb_layout& L, const double* u, int inst, double* mean,
+                        double* m2, int64_t count_before, cudaStream_t st);
+int launch_moments_merge(double* ma, double* m2a, int64_t ca, const double* mb, const double* m2b, int64_t cb,
+                         int64_t n, cudaStream_t st);
+int launch_structure(const fvb_scheme& s, const fvb_layout& L, const double* u, int inst, int comp, double p,
+                     int H, double* d_sums, double* d_partials, int nblocks, cudaStream_t st);
+int structure_blocks(const fvb_scheme& s);
+}  // namespace fvb
+
+using fvb::FvbState;
+using fvb::LoopCtl;
+using fvb::StageParams;
+
+struct RunPlan {
+  fvb_scheme s;
+  fvb_layout L;
+  double* bufs[3];
+  int ninst;
+  int mode;
+  int64_t max_steps;
+  int64_t steps_enqueued;
+  StageParams stage[3];  // per stage of a step (RK1 uses [0] with ping-pong)
+  int nstages;
+  dim3 grid;
+  int active;
+};
+
+struct fvb_ctx {
+  int device;
+  cudaStream_t stream;
+  char msg[1024];
+  FvbState* d_state;  // run state, one per instance
+  int state_cap;
+  FvbState* d_scratch_state;  // for single-shot calls
+  double2* d_log;
+  int64_t log_cap_alloc;  // allocated (t,dt) entries
+  int64_t log_stride;     // entries per instance for the current run (0 = no log)
+  double* d_partials;
+  int64_t partials_cap;
+  RunPlan plan;
+  cudaGraphExec_t graph;
+  int graph_steps;
+  int graph_parity_ok;
+  int64_t launches;
+};
+
+static int set_err(fvb_ctx* ctx, int code, const char* fmt, ...) {
+  if (ctx) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(ctx->msg, sizeof(ctx->msg), fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+
+#define CUDA_TRY(ctx, call)                                                              \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return set_err(ctx, FVB_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+static int check_launch(fvb_ctx* ctx, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(ctx, FVB_E_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
+  return FVB_OK;
+}
+
+static int validate(fvb_ctx* ctx, const fvb_scheme* s) {
+  if (!s) return set_err(ctx, FVB_E_CONFIG, "null scheme");
+  if (s->dim < 1 || s->dim > 3) return set_err(ctx, FVB_E_CONFIG, "dim must be 1, 2 or 3, got %d", s->dim);
+  if (s->eq < 0 || s->eq > 2) return set_err(ctx, FVB_E_CONFIG, "unknown equation kind %d", s->eq);
+  const int nc = s->eq == FVB_EQ_EULER ? s->dim + 2 : 1;
+  if (s->ncomp != nc) return set_err(ctx, FVB_E_CONFIG, "ncomp %d does not match the equation (%d)", s->ncomp, nc);
+  if (s->flux == FVB_FLUX_HLLC && s->eq != FVB_EQ_EULER)
+    return set_err(ctx, FVB_E_CONFIG, "HLLC flux requires the Euler equations");
+  if (s->rk_order < 1 || s->rk_order > 3)
+    return set_err(ctx, FVB_E_CONFIG, "rk_order must be 1, 2 or 3, got %d", s->rk_order);
+  const int radius = s->recon == FVB_RECON_NONE ? 1 : 2;
+  for (int k = 0; k < 3; ++k) {
+    if (k >= s->dim) continue;
+    if (s->cells[k] < 1) return set_err(ctx, FVB_E_CONFIG, "all cell counts must be >= 1");
+    if (s->bc[k] == FVB_BC_PERIODIC && s->cells[k] < radius)
+      return set_err(ctx, FVB_E_CONFIG, "periodic axis %d needs cells >= %d", k, radius);
+    if (s->bc[k] == FVB_BC_HALO && s->ghost < radius)
+      return set_err(ctx, FVB_E_CONFIG, "ghost_width %d too small for reconstruction radius %d", s->ghost, radius);
+  }
+  return FVB_OK;
+}
+
+static bool is_pow2(double d) {
+  int e;
+  const double m = std::frexp(d, &e);
+  return m == 0.5;
+}
+
+// Fill the geometry / physics part of a StageParams.
+static StageParams base_params(const fvb_scheme& s, const fvb_layout& L) {
+  StageParams p;
+  std::memset(&p, 0, sizeof(p));
+  for (int k = 0; k < 3; ++k) {
+    p.n[k] = k < s.dim ? s.cells[k] : 1;
+    p.bc[k] = k < s.dim ? s.bc[k] : FVB_BC_PERIODIC;
+    p.dd[k] = k < s.dim ? s.deltas[k] : 1.0;
+    p.id[k] = 1.0 / p.dd[k];
+    p.divd[k] = is_pow2(p.dd[k]) ? 0 : 1;
+  }
+  p.g = s.ghost;
+  p.origin = L.origin;
+  p.sy = L.sy;
+  p.sz = L.sz;
+  p.sc = L.sc;
+  p.si = L.si;
+  p.P.gamma = s.gamma;
+  p.P.gm1 = s.gamma - 1.0;
+  p.P.eps = s.weno_eps;
+  for (int k = 0; k < 3; ++k) p.P.adv[k] = s.adv[k];
+  p.ctl.dim = s.dim;
+  p.ctl.cfl = s.cfl;
+  p.ctl.t_end = s.t_end;
+  for (int k = 0; k < 3; ++k) p.ctl.deltas[k] = p.dd[k];
+  return p;
+}
+
+// Grid of the stage kernel; fills chunks / H / nblocks.
+static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst) {
+  int nt, nty;
+  if (s.arith == FVB_ARITH_FAST) fvb::fast::stage_block(s.dim, nt, nty);
+  else fvb::exact::stage_block(s.dim, nt, nty);
+  const int64_t strips = (p.n[0] + (nt - 2) - 1) / (nt - 2);
+  dim3 g(1, 1, 1);
+  g.x = (unsigned)strips;
+  int64_t H = 1, chunks = 1;
+  if (s.dim >= 2) {
+    const int64_t nm = p.n[s.dim - 1];
+    int64_t ytiles = 1;
+    if (s.dim == 3) ytiles = (p.n[1] + (nty - 2) - 1) / (nty - 2);
+    // aim for ~2 waves of resident blocks over 148 SMs
+    const int64_t per_sm = s.dim == 3 ? 1 : 6;
+    const int64_t target = 148 * per_sm * 2;
+    int64_t want_chunks = (target + strips * ytiles * ninst - 1) / (strips * ytiles * ninst);
+    want_chunks = std::max<int64_t>(1, std::min<int64_t>(want_chunks, nm));
+    H = (nm + want_chunks - 1) / want_chunks;
+    const char* env = getenv("FVB_MARCH_ROWS");
+    if (env && atoi(env) > 0) H = atoi(env);
+    H = std::max<int64_t>(4, std::min<int64_t>(H, nm));
+    chunks = (nm + H - 1) / H;
+    if (s.dim == 2) {
+      g.y = (unsigned)chunks;
+      g.z = ninst;
+    } else {
+      g.y = (unsigned)ytiles;
+      g.z = (unsigned)(chunks * ninst);
+    }
+  } else {
+    g.z = ninst;
+  }
+  p.H = (int)H;
+  p.chunks = (int)chunks;
+  p.nblocks = (unsigned)(g.x * g.y * (s.dim == 3 ? chunks : 1) * (s.dim == 2 ? chunks : 1));
+  if (s.dim == 2) p.nblocks = (unsigned)(g.x * chunks);
+  if (s.dim == 3) p.nblocks = (unsigned)(g.x * g.y * chunks);
+  if (s.dim == 1) p.nblocks = g.x;
+  return g;
+}
+
+static int do_stage(fvb_ctx* ctx, const fvb_scheme& s, const StageParams& p, dim3 grid) {
+  int r = s.arith == FVB_ARITH_FAST ? fvb::fast::launch_stage(s.dim, s.eq, s.flux, s.recon, p, grid, ctx->stream)
+                                    : fvb::exact::launch_stage(s.dim, s.eq, s.flux, s.recon, p, grid, ctx->stream);
+  if (r != 0) return set_err(ctx, FVB_E_CONFIG, "unsupported scheme combination");
+  ctx->launches++;
+  return check_launch(ctx, "stage_kernel");
+}
+
+static int do_speed(fvb_ctx* ctx, const fvb_scheme& s, const StageParams& p, int finalize, int ninst) {
+  const int64_t ncell = p.n[0] * p.n[1] * p.n[2];
+  int64_t blocks = (ncell + 255) / 256;
+  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 8 / std::max(1, ninst) + 1));
+  dim3 grid((unsigned)blocks, ninst, 1);
+  int r = s.arith == FVB_ARITH_FAST ? fvb::fast::launch_speed(s.dim, s.eq, p, finalize, grid, ctx->stream)
+                                    : fvb::exact::launch_speed(s.dim, s.eq, p, finalize, grid, ctx->stream);
+  if (r != 0) return set_err(ctx, FVB_E_CONFIG, "unsupported dim");
+  ctx->launches++;
+  return check_launch(ctx, "speed_kernel");
+}
+
+static void init_state_host(FvbState& h) {
+  std::memset(&h, 0, sizeof(h));
+  h.bad_nonfinite = fvb::kNone;
+  h.bad_unphys = fvb::kNone;
+  h.stage_err = fvb::kNone;
+}
+
+static int ensure_state(fvb_ctx* ctx, int ninst) {
+  if (ninst <= ctx->state_cap) return FVB_OK;
+  if (ctx->d_state) cudaFree(ctx->d_state);
+  ctx->d_state = nullptr;
+  CUDA_TRY(ctx, cudaMalloc(&ctx->d_state, sizeof(FvbState) * ninst));
+  ctx->state_cap = ninst;
+  return FVB_OK;
+}
+
+static int reset_states(fvb_ctx* ctx, FvbState* d, int ninst, double dt) {
+  std::vector<FvbState> h(ninst);
+  for (auto& x : h) {
+    init_state_host(x);
+    x.dt = dt;
+  }
+  CUDA_TRY(ctx, cudaMemcpyAsync(d, h.data(), sizeof(FvbState) * ninst, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return FVB_OK;
+}
+
+static void destroy_graph(fvb_ctx* ctx) {
+  if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+  ctx->graph = nullptr;
+}
+
+static int ensure_log(fvb_ctx* ctx, int64_t n) {
+  if (n <= ctx->log_cap_alloc) return FVB_OK;
+  if (ctx->d_log) cudaFree(ctx->d_log);
+  ctx->d_log = nullptr;
+  CUDA_TRY(ctx, cudaMalloc(&ctx->d_log, sizeof(double2) * n));
+  ctx->log_cap_alloc = n;
+  return FVB_OK;
+}
+
+extern "C" {
+
+int fvb_version(void) { return 1; }
+
+int fvb_ctx_create(int device, void* stream, fvb_ctx** out) {
+  if (!out) return FVB_E_CONFIG;
+  fvb_ctx* ctx = new fvb_ctx;
+  std::memset(ctx, 0, sizeof(*ctx));
+  ctx->device = device;
+  ctx->stream = (cudaStream_t)stream;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    *out = ctx;
+    return set_err(ctx, FVB_E_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+  }
+  e = cudaMalloc(&ctx->d_scratch_state, sizeof(FvbState) * 4096);
+  if (e != cudaSuccess) {
+    *out = ctx;
+    return set_err(ctx, FVB_E_CUDA, "cudaMalloc: %s", cudaGetErrorString(e));
+  }
+  *out = ctx;
+  return FVB_OK;
+}
+
+int fvb_ctx_destroy(fvb_ctx* ctx) {
+  if (!ctx) return FVB_OK;
+  destroy_graph(ctx);
+  if (ctx->d_state) cudaFree(ctx->d_state);
+  if (ctx->d_scratch_state) cudaFree(ctx->d_scratch_state);
+  if (ctx->d_log) cudaFree(ctx->d_log);
+  if (ctx->d_partials) cudaFree(ctx->d_partials);
+  delete ctx;
+  return FVB_OK;
+}
+
+int fvb_ctx_set_stream(fvb_ctx* ctx, void* stream) {
+  if (ctx->stream != (cudaStream_t)stream) destroy_graph(ctx);
+  ctx->stream = (cudaStream_t)stream;
+  return FVB_OK;
+}
+
+int fvb_last_error(const fvb_ctx* ctx, char* buf, size_t n) {
+  if (!ctx || !buf || n == 0) return FVB_E_CONFIG;
+  std::snprintf(buf, n, "%s", ctx->msg);
+  return FVB_OK;
+}
+
+int fvb_sync(fvb_ctx* ctx) {
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return FVB_OK;
+}
+
+int64_t fvb_launch_count(const fvb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int fvb_fill_ghosts(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, double* u, int ninst) {
+  int r = validate(ctx, s);
+  if (r) return r;
+  for (int axis = 0; axis < s->dim; ++axis) {
+    if (s->bc[axis] == FVB_BC_PERIODIC && s->cells[axis] < s->ghost)
+      return set_err(ctx, FVB_E_CONFIG, "periodic axis %d needs cells >= ghost_width (%lld < %d)", axis,
+                     (long long)s->cells[axis], s->ghost);
+    if (s->bc[axis] == FVB_BC_HALO) continue;
+    fvb::launch_fill_axis(*s, *lay, u, ninst, axis, ctx->stream);
+    ctx->launches++;
+    r = check_launch(ctx, "fill_axis");
+    if (r) return r;
+  }
+  return FVB_OK;
+}
+
+int fvb_wave_speed_maxima(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, const double* u, int ninst,
+                          double* h_max) {
+  int r = validate(ctx, s);
+  if (r) return r;
+  if (ninst > 4096) return set_err(ctx, FVB_E_CONFIG, "too many instances");
+  r = reset_states(ctx, ctx->d_scratch_state, ninst, 0.0);
+  if (r) return r;
+  StageParams p = base_params(*s, *lay);
+  p.us = u;
+  p.st = ctx->d_scratch_state;
+  r = do_speed(ctx, *s, p, 0, ninst);
+  if (r) return r;
+  std::vector<FvbState> h(ninst);
+  CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), ctx->d_scratch_state, sizeof(FvbState) * ninst, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < ninst; ++i) {
+    for (int k = 0; k < s->dim; ++k) {
+      double d;
+      std::memcpy(&d, &h[i].smax[k], 8);
+      h_max[i * s->dim + k] = d;
+    }
+    if (h[i].bad_unphys != fvb::kNone)
+      return set_err(ctx, FVB_E_UNPHYSICAL, "unphysical state at cell %lld (instance %d)",
+                     (long long)h[i].bad_unphys, i);
+  }
+  return FVB_OK;
+}
+
+static int stage_error(fvb_ctx* ctx, const FvbState& h, int inst) {
+  if (h.stage_err == fvb::kNone) return FVB_OK;
+  const int kind = (int)((h.stage_err >> 40) & 3);
+  const long long cell = h.stage_err & ((1LL << 40) - 1);
+  if (kind == 0)
+    return set_err(ctx, FVB_E_SIMULATION, "unphysical state in interior cell #%lld (instance %d)", cell, inst);
+  return set_err(ctx, FVB_E_UNPHYSICAL, "degenerate HLLC wave fan (sL >= sR)");
+}
+
+int fvb_spatial_residual(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, const double* u, double* out,
+                         int ninst) {
+  int r = validate(ctx, s);
+  if (r) return r;
+  r = reset_states(ctx, ctx->d_scratch_state, ninst, 0.0);
+  if (r) return r;
+  StageParams p = base_params(*s, *lay);
+  p.us = u;
+  p.un = u;
+  p.out = out;
+  p.st = ctx->d_scratch_state;
+  p.kind = 0;
+  dim3 g = stage_grid(*s, p, ninst);
+  r = do_stage(ctx, *s, p, g);
+  if (r) return r;
+  std::vector<FvbState> h(ninst);
+  CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), ctx->d_scratch_state, sizeof(FvbState) * ninst, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < ninst; ++i) {
+    r = stage_error(ctx, h[i], i);
+    if (r) return r;
+  }
+  return FVB_OK;
+}
+
+// Stage parameters of one SSP-RK step over buffers b (solver.py:164-173).
+static int build_step(const fvb_scheme& s, const fvb_layout& L, double* const b[3], StageParams base,
+                      StageParams out[3]) {
+  const int rk = s.rk_order;
+  for (int i = 0; i < 3; ++i) out[i] = base;
+  if (rk == 1) {
+    out[0].us = b[0]; out[0].un = b[0]; out[0].out = b[1]; out[0].kind = 1; out[0].final_stage = 1;
+    out[0].stage_idx = 0;
+    return 1;
+  }
+  if (rk == 2) {
+    out[0].us = b[0]; out[0].un = b[0]; out[0].out = b[1]; out[0].kind = 1; out[0].stage_idx = 0;
+    out[1].us = b[1]; out[1].un = b[0]; out[1].out = b[0]; out[1].kind = 2; out[1].final_stage = 1;
+    out[1].stage_idx = 1;
+    return 2;
+  }
+  out[0].us = b[0]; out[0].un = b[0]; out[0].out = b[1]; out[0].kind = 1; out[0].stage_idx = 0;
+  out[1].us = b[1]; out[1].un = b[0]; out[1].out = b[2]; out[1].kind = 3; out[1].stage_idx = 1;
+  out[2].us = b[2]; out[2].un = b[0]; out[2].out = b[0]; out[2].kind = 4; out[2].final_stage = 1;
+  out[2].stage_idx = 2;
+  return 3;
+}
+
+int fvb_ssp_rk_step(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, double* un, double* w1, double* w2,
+                    int ninst, double dt) {
+  int r = validate(ctx, s);
+  if (r) return r;
+  r = reset_states(ctx, ctx->d_scratch_state, ninst, dt);
+  if (r) return r;
+  StageParams base = base_params(*s, *lay);
+  base.st = ctx->d_scratch_state;
+  dim3 g = stage_grid(*s, base, ninst);
+  double* b[3] = {un, w1, w2};
+  StageParams st[3];
+  const int ns = build_step(*s, *lay, b, base, st);
+  for (int i = 0; i < ns; ++i) {
+    st[i].final_stage = 0;  // ssp_rk_step has no post-step checks (solver.py:176-196)
+    r = do_stage(ctx, *s, st[i], g);
+    if (r) return r;
+  }
+  if (s->rk_order == 1) {
+    // result is in w1: copy back into un (interior and ghosts alike)
+    const int64_t total = (int64_t)ninst * (lay->si ? lay->si : (lay->sc * s->ncomp));
+    CUDA_TRY(ctx, cudaMemcpyAsync(un, w1, sizeof(double) * total, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  std::vector<FvbState> h(ninst);
+  CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), ctx->d_scratch_state, sizeof(FvbState) * ninst, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < ninst; ++i) {
+    r = stage_error(ctx, h[i], i);
+    if (r) return r;
+  }
+  return FVB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Device-resident run loop
+// ---------------------------------------------------------------------------
+
+static int enqueue_step(fvb_ctx* ctx) {
+  RunPlan& P = ctx->plan;
+  if (P.s.rk_order == 1) {
+    StageParams p = P.stage[0];
+    const int par = (int)(P.steps_enqueued & 1);
+    p.us = P.bufs[par];
+    p.un = P.bufs[par];
+    p.out = P.bufs[1 - par];
+    int r = do_stage(ctx, P.s, p, P.grid);
+    if (r) return r;
+  } else {
+    for (int i = 0; i < P.nstages; ++i) {
+      int r = do_stage(ctx, P.s, P.stage[i], P.grid);
+      if (r) return r;
+    }
+  }
+  P.steps_enqueued++;
+  return FVB_OK;
+}
+
+int fvb_run_begin(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, double* bufs[3], int ninst, int mode,
+                  int64_t max_steps) {
+  int r = validate(ctx, s);
+  if (r) return r;
+  destroy_graph(ctx);
+  ctx->launches = 0;
+  r = ensure_state(ctx, ninst);
+  if (r) return r;
+  r = reset_states(ctx, ctx->d_state, ninst, 0.0);
+  if (r) return r;
+  RunPlan& P = ctx->plan;
+  std::memset(&P, 0, sizeof(P));
+  P.s = *s;
+  P.L = *lay;
+  for (int i = 0; i < 3; ++i) P.bufs[i] = bufs[i];
+  P.ninst = ninst;
+  P.mode = mode;
+  P.max_steps = max_steps;
+  StageParams base = base_params(*s, *lay);
+  base.st = ctx->d_state;
+  base.ctl.mode = mode;
+  base.ctl.max_steps = mode == FVB_MODE_FIXED ? max_steps : max_steps;
+  base.ctl.log = ctx->log_stride > 0 ? ctx->d_log : nullptr;
+  base.ctl.log_cap = ctx->log_stride;
+  P.grid = stage_grid(*s, base, ninst);
+  P.nstages = build_step(*s, *lay, P.bufs, base, P.stage);
+  P.active = 1;
+  // initial wave-speed pass + first dt (solver.py:211-224)
+  StageParams sp = base;
+  sp.us = bufs[0];
+  return do_speed(ctx, *s, sp, 1, ninst);
+}
+
+int fvb_run_steps(fvb_ctx* ctx, int64_t n_steps) {
+  RunPlan& P = ctx->plan;
+  if (!P.active) return set_err(ctx, FVB_E_CONFIG, "fvb_run_steps without fvb_run_begin");
+  const char* env = getenv("FVB_GRAPH_STEPS");
+  int gs = ctx->graph_steps > 0 ? ctx->graph_steps : 16;
+  if (env && atoi(env) >= 0) gs = atoi(env);
+  if (P.s.rk_order == 1 && (gs & 1)) gs += 1;
+  int64_t left = n_steps;
+  if (P.s.rk_order == 1 && (P.steps_enqueued & 1) && left > 0) {
+    int r = enqueue_step(ctx);
+    if (r) return r;
+    --left;
+  }
+  if (gs > 1 && left >= gs) {
+    if (!ctx->graph) {
+      cudaGraph_t graph;
+      CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      const int64_t saved = P.steps_enqueued;
+      const int64_t saved_l = ctx->launches;
+      for (int i = 0; i < gs; ++i) {
+        int r = enqueue_step(ctx);
+        if (r) {
+          cudaStreamEndCapture(ctx->stream, &graph);
+          return r;
+        }
+      }
+      P.steps_enqueued = saved;
+      ctx->launches = saved_l;
+      CUDA_TRY(ctx, cudaStreamEndCapture(ctx->stream, &graph));
+      CUDA_TRY(ctx, cudaGraphInstantiate(&ctx->graph, graph, 0));
+      cudaGraphDestroy(graph);
+      ctx->graph_steps = gs;
+    }
+    while (left >= ctx->graph_steps) {
+      CUDA_TRY(ctx, cudaGraphLaunch(ctx->graph, ctx->stream));
+      P.steps_enqueued += ctx->graph_steps;
+      ctx->launches += (int64_t)ctx->graph_steps * (P.s.rk_order == 1 ? 1 : P.nstages);
+      left -= ctx->graph_steps;
+    }
+  }
+  while (left > 0) {
+    int r = enqueue_step(ctx);
+    if (r) return r;
+    --left;
+  }
+  return FVB_OK;
+}
+
+static int state_to_info(fvb_ctx* ctx, const FvbState& h, fvb_run_info* info) {
+  info->t = h.t;
+  info->dt = h.dt;
+  info->steps = h.step;
+  info->err = h.err;
+  info->errsub = h.errsub;
+  info->errcell = h.errcell;
+  return FVB_OK;
+}
+
+int fvb_run_poll(fvb_ctx* ctx, fvb_run_info* h_info, int32_t* h_done) {
+  RunPlan& P = ctx->plan;
+  if (!P.active) return set_err(ctx, FVB_E_CONFIG, "fvb_run_poll without fvb_run_begin");
+  std::vector<FvbState> h(P.ninst);
+  CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), ctx->d_state, sizeof(FvbState) * P.ninst, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < P.ninst; ++i) {
+    if (h_info) state_to_info(ctx, h[i], h_info + i);
+    if (h_done) h_done[i] = h[i].done;
+  }
+  return FVB_OK;
+}
+
+int fvb_run_read_log(fvb_ctx* ctx, double* h_log, int64_t per_instance) {
+  RunPlan& P = ctx->plan;
+  if (!P.active || ctx->log_stride <= 0) return set_err(ctx, FVB_E_CONFIG, "no active step log");
+  if (per_instance != ctx->log_stride) return set_err(ctx, FVB_E_CONFIG, "log size mismatch");
+  CUDA_TRY(ctx, cudaMemcpyAsync(h_log, ctx->d_log, sizeof(double2) * per_instance * P.ninst, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return FVB_OK;
+}
+
+int fvb_run_set_log(fvb_ctx* ctx, int64_t per_instance, int ninst) {
+  if (per_instance <= 0) {
+    ctx->log_stride = 0;
+    return FVB_OK;
+  }
+  int r = ensure_log(ctx, per_instance * ninst);
+  if (r) return r;
+  ctx->log_stride = per_instance;
+  return FVB_OK;
+}
+
+int fvb_run_end(fvb_ctx* ctx, fvb_run_info* h_info, double* h_log, int64_t log_cap) {
+  RunPlan& P = ctx->plan;
+  if (!P.active) return set_err(ctx, FVB_E_CONFIG, "fvb_run_end without fvb_run_begin");
+  std::vector<FvbState> h(P.ninst);
+  CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), ctx->d_state, sizeof(FvbState) * P.ninst, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  int first_err = FVB_OK;
+  for (int i = 0; i < P.ninst; ++i) {
+    if (h_info) state_to_info(ctx, h[i], h_info + i);
+    if (h[i].err && !first_err) first_err = h[i].err;
+  }
+  if (h_log && log_cap > 0 && ctx->d_log && ctx->log_stride > 0) {
+    const int64_t cap = std::min<int64_t>(log_cap, ctx->log_stride);
+    for (int i = 0; i < P.ninst; ++i) {
+      CUDA_TRY(ctx, cudaMemcpyAsync(h_log + 2 * i * log_cap, ctx->d_log + i * ctx->log_stride,
+                                    sizeof(double2) * cap, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  P.active = 0;
+  if (first_err) return set_err(ctx, first_err, "run failed (see run info)");
+  return FVB_OK;
+}
+
+int fvb_run(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, double* bufs[3], int ninst, int mode,
+            int64_t max_steps, double* h_log, int64_t log_cap, int graph_steps, fvb_run_info* h_info) {
+  int r = ensure_log(ctx, log_cap > 0 ? log_cap * ninst : 0);
+  if (r) return r;
+  ctx->log_stride = (h_log && log_cap > 0) ? log_cap : 0;
+  ctx->graph_steps = graph_steps;
+  r = fvb_run_begin(ctx, s, lay, bufs, ninst, mode, max_steps);
+  if (r) return r;
+  RunPlan& P = ctx->plan;
+  std::vector<FvbState> h(ninst);
+  int64_t batch = graph_steps > 0 ? graph_steps : 16;
+  for (;;) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), ctx->d_state, sizeof(FvbState) * ninst, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    bool all_done = true;
+    double est = 0;
+    for (int i = 0; i < ninst; ++i) {
+      if (!h[i].done) {
+        all_done = false;
+        if (mode == FVB_MODE_T_END && h[i].dt > 0) est = std::max(est, (s->t_end - h[i].t) / h[i].dt);
+      }
+    }
+    if (all_done) break;
+    int64_t n = batch;
+    if (mode == FVB_MODE_FIXED) n = std::max<int64_t>(1, max_steps - P.steps_enqueued);
+    else if (max_steps >= 0) n = std::max<int64_t>(1, std::min<int64_t>(n, max_steps - P.steps_enqueued));
+    r = fvb_run_steps(ctx, n);
+    if (r) return r;
+  }
+  r = fvb_run_end(ctx, h_info, h_log, log_cap);
+  ctx->log_stride = 0;
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// UQ statistics and halo slabs (kernels in fvb_aux.cu)
+// ---------------------------------------------------------------------------
+
+int fvb_moments_push(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, const double* u, int inst,
+                     double* mean, double* m2, int64_t count_before) {
+  fvb::launch_moments_push(*s, *lay, u, inst, mean, m2, count_before, ctx->stream);
+  ctx->launches++;
+  return check_launch(ctx, "moments_push");
+}
+
+int fvb_moments_merge(fvb_ctx* ctx, double* mean_a, double* m2_a, int64_t count_a, const double* mean_b,
+                      const double* m2_b, int64_t count_b, int64_t n) {
+  fvb::launch_moments_merge(mean_a, m2_a, count_a, mean_b, m2_b, count_b, n, ctx->stream);
+  ctx->launches++;
+  return check_launch(ctx, "moments_merge");
+}
+
+int fvb_structure_push(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, const double* u, int inst,
+                       int comp, double p, int H, double* d_sums) {
+  if (H < 0 || H > 63) return set_err(ctx, FVB_E_CONFIG, "structure_max_offset must lie in [0, 63], got %d", H);
+  const int nb = fvb::structure_blocks(*s);
+  const int64_t need = (int64_t)nb * (H + 1) * s->dim;
+  if (need > ctx->partials_cap) {
+    if (ctx->d_partials) cudaFree(ctx->d_partials);
+    ctx->d_partials = nullptr;
+    CUDA_TRY(ctx, cudaMalloc(&ctx->d_partials, sizeof(double) * need));
+    ctx->partials_cap = need;
+  }
+  fvb::launch_structure(*s, *lay, u, inst, comp, p, H, d_sums, ctx->d_partials, nb, ctx->stream);
+  ctx->launches += 2;
+  return check_launch(ctx, "structure_push");
+}
+
+int fvb_halo_pack(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, const double* u, int axis, int side,
+                  double* buf) {
+  fvb::launch_halo(*s, *lay, const_cast<double*>(u), axis, side, buf, 0, ctx->stream);
+  ctx->launches++;
+  return check_launch(ctx, "halo_pack");
+}
+
+int fvb_halo_unpack(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, double* u, int axis, int side,
+                    const double* buf) {
+  fvb::launch_halo(*s, *lay, u, axis, side, const_cast<double*>(buf), 1, ctx->stream);
+  ctx->launches++;
+  return check_launch(ctx, "halo_unpack");
+}
+
+int64_t fvb_halo_count(const fvb_scheme* s, int axis) { return fvb::halo_count(*s, axis); }
+
+}  // extern "C"

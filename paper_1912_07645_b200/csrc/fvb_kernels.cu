@@ -1,0 +1,82 @@
+// Instantiates the stage / wave-speed kernels for one arithmetic mode.
+// Built twice: -DFVB_FAST=0 -DFVB_NS=exact -fmad=false  (bitwise == reference)
+//              -DFVB_FAST=1 -DFVB_NS=fast  -fmad=true
+#include "fvb_stage.cuh"
+
+namespace fvb {
+namespace FVB_NS {
+
+template <int DIM> struct Blk;
+template <> struct Blk<1> { static constexpr int NT = 128, NTY = 1; };
+template <> struct Blk<2> { static constexpr int NT = 64, NTY = 1; };
+template <> struct Blk<3> { static constexpr int NT = 32, NTY = 8; };
+
+void stage_block(int dim, int& nt, int& nty) {
+  if (dim == 1) { nt = Blk<1>::NT; nty = Blk<1>::NTY; }
+  else if (dim == 2) { nt = Blk<2>::NT; nty = Blk<2>::NTY; }
+  else { nt = Blk<3>::NT; nty = Blk<3>::NTY; }
+}
+
+template <int DIM, int EQ, int FLUX, int RECON>
+static int launch_one(const StageParams& p, dim3 grid, cudaStream_t s) {
+  constexpr int NT = Blk<DIM>::NT, NTY = Blk<DIM>::NTY;
+  constexpr int smem = stage_smem_bytes<DIM, EQ, RECON, NT, NTY>();
+  auto kern = stage_kernel<DIM, EQ, FLUX, RECON, NT, NTY>;
+  static bool attr_done = false;  // per instantiation
+  if (!attr_done) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_done = true;
+  }
+  kern<<<grid, dim3(NT, NTY), smem, s>>>(p);
+  return 0;
+}
+
+template <int DIM>
+static int launch_dim(int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s) {
+#define FVB_CASE(E, F, R) \
+  if (eq == E && flux == F && recon == R) return launch_one<DIM, E, F, R>(p, grid, s);
+  FVB_CASE(EQ_EULER, FLUX_HLLC, RECON_NONE)
+  FVB_CASE(EQ_EULER, FLUX_HLLC, RECON_WENO2)
+  FVB_CASE(EQ_EULER, FLUX_HLLC, RECON_WENO3)
+  FVB_CASE(EQ_EULER, FLUX_RUSANOV, RECON_NONE)
+  FVB_CASE(EQ_EULER, FLUX_RUSANOV, RECON_WENO2)
+  FVB_CASE(EQ_EULER, FLUX_RUSANOV, RECON_WENO3)
+  FVB_CASE(EQ_BURGERS, FLUX_RUSANOV, RECON_NONE)
+  FVB_CASE(EQ_BURGERS, FLUX_RUSANOV, RECON_WENO2)
+  FVB_CASE(EQ_BURGERS, FLUX_RUSANOV, RECON_WENO3)
+  FVB_CASE(EQ_ADVECTION, FLUX_RUSANOV, RECON_NONE)
+  FVB_CASE(EQ_ADVECTION, FLUX_RUSANOV, RECON_WENO2)
+  FVB_CASE(EQ_ADVECTION, FLUX_RUSANOV, RECON_WENO3)
+#undef FVB_CASE
+  return -1;
+}
+
+int launch_stage(int dim, int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s) {
+  switch (dim) {
+    case 1: return launch_dim<1>(eq, flux, recon, p, grid, s);
+    case 2: return launch_dim<2>(eq, flux, recon, p, grid, s);
+    case 3: return launch_dim<3>(eq, flux, recon, p, grid, s);
+  }
+  return -1;
+}
+
+template <int DIM>
+static int launch_speed_dim(int eq, const StageParams& p, int fin, dim3 grid, cudaStream_t s) {
+  if (eq == EQ_EULER) speed_kernel<DIM, EQ_EULER><<<grid, 256, 0, s>>>(p, fin);
+  else if (eq == EQ_BURGERS) speed_kernel<DIM, EQ_BURGERS><<<grid, 256, 0, s>>>(p, fin);
+  else speed_kernel<DIM, EQ_ADVECTION><<<grid, 256, 0, s>>>(p, fin);
+  return 0;
+}
+
+int launch_speed(int dim, int eq, const StageParams& p, int fin, dim3 grid, cudaStream_t s) {
+  switch (dim) {
+    case 1: return launch_speed_dim<1>(eq, p, fin, grid, s);
+    case 2: return launch_speed_dim<2>(eq, p, fin, grid, s);
+    case 3: return launch_speed_dim<3>(eq, p, fin, grid, s);
+  }
+  return -1;
+}
+
+}  // namespace FVB_NS
+}  // namespace fvb

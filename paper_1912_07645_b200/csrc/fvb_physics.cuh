@@ -1,0 +1,303 @@
+// Device-side physics for the finite-volume stage: equation of state,
+// physical fluxes, wave speeds, WENO2/3 face reconstruction, Rusanov and
+// HLLC numerical fluxes.
+//
+// Two arithmetic modes share this header:
+//   FVB_FAST == 0  "exact": compiled with -fmad=false and written in the
+//                  reference's operation order, so every value is bitwise
+//                  identical to numpy (one IEEE binary64 op per numpy pass).
+//   FVB_FAST == 1  "fast": same algorithm, algebraically restructured to
+//                  remove divides (one reciprocal per WENO pair, 1/rho per
+//                  state) and FMA-contracted; parity is relative L1 <= 1e-12
+//                  over the test windows.
+//
+// Reference citations: /root/reference/pkg/src/conslaw/<file>:<line>.
+#pragma once
+#include <cstdint>
+#include <cmath>
+#include "fvb_common.cuh"
+
+#ifndef FVB_FAST
+#error "FVB_FAST must be defined to 0 or 1"
+#endif
+
+namespace fvb {
+
+// numpy.maximum / numpy.minimum: NaN-propagating (numerics.py:138,164-165)
+__device__ __forceinline__ double np_max(double a, double b) { return (a > b || a != a) ? a : b; }
+__device__ __forceinline__ double np_min(double a, double b) { return (a < b || a != a) ? a : b; }
+
+// ---------------------------------------------------------------------------
+// Euler equation of state (equations.py:62-73, 128-129)
+// ---------------------------------------------------------------------------
+template <int DIM>
+__device__ __forceinline__ double euler_pressure(const double* u, const Phys& P) {
+  // sum(m_k**2) starts from int 0 in the reference: 0 + m0^2 == m0^2 exactly
+  double msq = u[1] * u[1];
+#pragma unroll
+  for (int k = 1; k < DIM; ++k) msq = msq + u[1 + k] * u[1 + k];
+#if FVB_FAST
+  return P.gm1 * (u[1 + DIM] - msq * (0.5 / u[0]));
+#else
+  return P.gm1 * (u[1 + DIM] - msq / (2.0 * u[0]));
+#endif
+}
+
+template <int DIM>
+__device__ __forceinline__ bool euler_physical(const double* u, const Phys& P) {
+  return (u[0] > kFloor) & (euler_pressure<DIM>(u, P) > kFloor);
+}
+
+// Physical flux F_axis(u) (equations.py:91-110), given p.
+template <int DIM>
+__device__ __forceinline__ void euler_flux(const double* u, double p, double v, int axis, double* f) {
+  f[0] = u[1 + axis];
+#pragma unroll
+  for (int j = 0; j < DIM; ++j) f[1 + j] = u[1 + j] * v;
+  f[1 + axis] = f[1 + axis] + p;
+  f[1 + DIM] = (u[1 + DIM] + p) * v;
+}
+
+// Per-state quantities shared by flux, wave speed and HLLC.
+struct EState { double rho, v, p, c; };
+
+template <int DIM>
+__device__ __forceinline__ EState euler_state(const double* u, int axis, const Phys& P) {
+  EState s;
+  s.rho = u[0];
+#if FVB_FAST
+  const double r = 1.0 / u[0];
+  s.v = u[1 + axis] * r;
+  double msq = u[1] * u[1];
+#pragma unroll
+  for (int k = 1; k < DIM; ++k) msq = fma(u[1 + k], u[1 + k], msq);
+  s.p = P.gm1 * (u[1 + DIM] - 0.5 * msq * r);
+  s.c = sqrt(P.gamma * s.p * r);
+#else
+  s.v = u[1 + axis] / s.rho;                      // numerics.py:159
+  s.p = euler_pressure<DIM>(u, P);                // numerics.py:160
+  s.c = sqrt(P.gamma * s.p / s.rho);              // equations.py:128-129
+#endif
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// WENO face reconstruction of one component (numerics.py:64-87, 109-117)
+//
+// For a cell with neighbours (um, uc, up) along the axis, returns the value
+// at its high face (uL of the interface to its right) and at its low face
+// (uR of the interface to its left).  The reference computes the low face
+// with the mirrored stencil (up, uc, um); with D0 = uc-um, D1 = up-uc the
+// mirrored smoothness indicators are (D1^2, D0^2) bitwise, so both faces
+// share beta, (eps+beta)^2 and -- for WENO2's symmetric ideal weights -- the
+// normalised weights themselves.  All shares are exact (negation, swap of a
+// commutative add), so the exact mode stays bitwise.
+// ---------------------------------------------------------------------------
+template <int RECON>
+__device__ __forceinline__ void weno_faces(double um, double uc, double up, double eps,
+                                           double& hi, double& lo) {
+  if constexpr (RECON == RECON_NONE) {
+    hi = uc;
+    lo = uc;
+  } else {
+    const double D0 = uc - um;
+    const double D1 = up - uc;
+#if FVB_FAST
+    const double e0 = fma(D0, D0, eps);
+    const double e1 = fma(D1, D1, eps);
+    const double q0 = e0 * e0;
+    const double q1 = e1 * e1;
+    if constexpr (RECON == RECON_WENO2) {
+      // w0 = q1/(q0+q1), w1 = q0/(q0+q1)
+      const double h = (0.5 / (q0 + q1)) * fma(q1, D0, q0 * D1);
+      hi = uc + h;
+      lo = uc - h;
+    } else {
+      // high face: a0 = (1/3)/q0, a1 = (2/3)/q1 -> w0 = q1/(q1 + 2 q0)
+      // low face : a0 = (1/3)/q1, a1 = (2/3)/q0 -> w0' = q0/(q0 + 2 q1)
+      const double th = fma(q1, D0, 2.0 * q0 * D1) / fma(2.0, q0, q1);
+      const double tl = fma(q0, D1, 2.0 * q1 * D0) / fma(2.0, q1, q0);
+      hi = fma(0.5, th, uc);
+      lo = fma(-0.5, tl, uc);
+    }
+#else
+    const double e0 = eps + D0 * D0;
+    const double e1 = eps + D1 * D1;
+    const double q0 = e0 * e0;
+    const double q1 = e1 * e1;
+    if constexpr (RECON == RECON_WENO2) {
+      const double a0 = 0.5 / q0;
+      const double a1 = 0.5 / q1;
+      const double s = a0 + a1;
+      const double w0 = a0 / s;
+      const double w1 = a1 / s;
+      const double S = w0 * D0 + w1 * D1;
+      const double h = 0.5 * S;
+      hi = uc + h;
+      lo = uc - h;
+    } else {
+      constexpr double d0 = 1.0 / 3.0, d1 = 2.0 / 3.0;  // numerics.py:53
+      const double a0 = d0 / q0, a1 = d1 / q1;
+      const double s = a0 + a1;
+      const double w0 = a0 / s, w1 = a1 / s;
+      hi = uc + 0.5 * (w0 * D0 + w1 * D1);
+      const double b0 = d0 / q1, b1 = d1 / q0;   // mirrored stencil
+      const double t = b0 + b1;
+      const double v0 = b0 / t, v1 = b1 / t;
+      lo = uc - 0.5 * (v0 * D1 + v1 * D0);
+    }
+#endif
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Numerical fluxes.  Error bit 1 = degenerate HLLC fan (numerics.py:166-167).
+// ---------------------------------------------------------------------------
+
+// Rusanov (numerics.py:133-142)
+template <int EQ, int DIM>
+__device__ __forceinline__ void rusanov(const double* uL, const double* uR, int axis,
+                                        const Phys& P, double* F) {
+  constexpr int NC = NComp<EQ, DIM>::value;
+  if constexpr (EQ == EQ_EULER) {
+    const EState L = euler_state<DIM>(uL, axis, P);
+    const EState R = euler_state<DIM>(uR, axis, P);
+    double fL[NC], fR[NC];
+    euler_flux<DIM>(uL, L.p, L.v, axis, fL);
+    euler_flux<DIM>(uR, R.p, R.v, axis, fR);
+    const double s = np_max(fabs(L.v) + L.c, fabs(R.v) + R.c);
+    const double hs = 0.5 * s;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) F[c] = 0.5 * (fL[c] + fR[c]) - hs * (uR[c] - uL[c]);
+  } else if constexpr (EQ == EQ_BURGERS) {
+    const double fL = 0.5 * uL[0] * uL[0];
+    const double fR = 0.5 * uR[0] * uR[0];
+    const double s = np_max(fabs(uL[0]), fabs(uR[0]));
+    F[0] = 0.5 * (fL + fR) - 0.5 * s * (uR[0] - uL[0]);
+  } else {
+    const double a = P.adv[axis];
+    const double fL = a * uL[0];
+    const double fR = a * uR[0];
+    const double s = fabs(a);
+    F[0] = 0.5 * (fL + fR) - 0.5 * s * (uR[0] - uL[0]);
+  }
+}
+
+// HLLC with Davis speeds (numerics.py:145-196).  Only the selected branch of
+// the reference's nested np.where is evaluated; the selected value is the
+// same expression, so results are identical.
+template <int DIM>
+__device__ __forceinline__ void hllc(const double* uL, const double* uR, int axis,
+                                     const Phys& P, double* F, unsigned& errbits) {
+  constexpr int NC = DIM + 2;
+  const EState L = euler_state<DIM>(uL, axis, P);
+  const EState R = euler_state<DIM>(uR, axis, P);
+  const double sL = np_min(L.v - L.c, R.v - R.c);
+  const double sR = np_max(L.v + L.c, R.v + R.c);
+  if (sR - sL <= 0.0) errbits |= 1u;
+
+  bool equal = true;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) equal &= (uL[c] == uR[c]);
+
+  if (equal || sL >= 0.0) {
+    euler_flux<DIM>(uL, L.p, L.v, axis, F);
+    return;
+  }
+  const double den = L.rho * (sL - L.v) - R.rho * (sR - R.v);
+#if FVB_FAST
+  const double sM = (fma(L.rho * L.v, sL - L.v, R.p - L.p) - R.rho * R.v * (sR - R.v)) / den;
+#else
+  const double sM = (R.p - L.p + L.rho * L.v * (sL - L.v) - R.rho * R.v * (sR - R.v)) / den;
+#endif
+  const double* u;
+  const EState* S;
+  double sK;
+  if (sM >= 0.0) {
+    u = uL; S = &L; sK = sL;
+  } else if (sR > 0.0) {
+    u = uR; S = &R; sK = sR;
+  } else {
+    euler_flux<DIM>(uR, R.p, R.v, axis, F);
+    return;
+  }
+  double f[NC];
+  euler_flux<DIM>(u, S->p, S->v, axis, f);
+  // star state (numerics.py:173-181)
+  double st[NC];
+#if FVB_FAST
+  const double sKv = sK - S->v;
+  const double rs = S->rho * sKv;
+  const double fac = rs / (sK - sM);
+  const double rinv = 1.0 / S->rho;
+  st[0] = fac;
+#pragma unroll
+  for (int j = 0; j < DIM; ++j) st[1 + j] = fac * (u[1 + j] * rinv);
+  st[1 + axis] = fac * sM;
+  st[1 + DIM] = fac * fma(sM - S->v, sM + S->p / rs, u[1 + DIM] * rinv);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) F[c] = fma(sK, st[c] - u[c], f[c]);
+#else
+  const double fac = S->rho * (sK - S->v) / (sK - sM);
+  st[0] = fac;
+#pragma unroll
+  for (int j = 0; j < DIM; ++j) {
+    if (j != axis) st[1 + j] = fac * (u[1 + j] / S->rho);
+  }
+  st[1 + axis] = fac * sM;
+  st[1 + DIM] = fac * (u[1 + DIM] / S->rho + (sM - S->v) * (sM + S->p / (S->rho * (sK - S->v))));
+#pragma unroll
+  for (int c = 0; c < NC; ++c) F[c] = f[c] + sK * (st[c] - u[c]);
+#endif
+}
+
+// Positivity fallback (solver.py:116-125): Euler + WENO only.  If either
+// reconstructed state is unphysical, both become the adjacent cell values.
+template <int EQ, int DIM, int RECON>
+__device__ __forceinline__ void fallback(double* uL, double* uR, const double* cL, const double* cR,
+                                         const Phys& P) {
+  if constexpr (EQ == EQ_EULER && RECON != RECON_NONE) {
+    constexpr int NC = DIM + 2;
+    if (!(euler_physical<DIM>(uL, P) & euler_physical<DIM>(uR, P))) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) { uL[c] = cL[c]; uR[c] = cR[c]; }
+    }
+  }
+}
+
+template <int EQ, int FLUX, int DIM>
+__device__ __forceinline__ void num_flux(const double* uL, const double* uR, int axis,
+                                         const Phys& P, double* F, unsigned& errbits) {
+  if constexpr (FLUX == FLUX_HLLC && EQ == EQ_EULER) {
+    hllc<DIM>(uL, uR, axis, P, F, errbits);
+  } else {
+    rusanov<EQ, DIM>(uL, uR, axis, P, F);
+  }
+}
+
+// Max wave speed of one state along every axis (equations.py:113-125)
+template <int EQ, int DIM>
+__device__ __forceinline__ void wave_speeds(const double* u, const Phys& P, double* s) {
+  if constexpr (EQ == EQ_EULER) {
+#if FVB_FAST
+    const double r = 1.0 / u[0];
+    const double p = euler_pressure<DIM>(u, P);
+    const double c = sqrt(P.gamma * p * r);
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) s[k] = fabs(u[1 + k] * r) + c;
+#else
+    const double p = euler_pressure<DIM>(u, P);
+    const double c = sqrt(P.gamma * p / u[0]);
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) s[k] = fabs(u[1 + k] / u[0]) + c;
+#endif
+  } else if constexpr (EQ == EQ_BURGERS) {
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) s[k] = fabs(u[0]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) s[k] = fabs(P.adv[k]);
+  }
+}
+
+}  // namespace fvb

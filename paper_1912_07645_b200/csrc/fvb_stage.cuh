@@ -1,0 +1,495 @@
+// Fused finite-volume stage kernel: WENO2/3 (or piecewise-constant) face
+// reconstruction + positivity fallback + Rusanov/HLLC flux + flux
+// difference + SSP-RK stage combination + (last stage) post-step checks and
+// the CFL wave-speed reduction, in ONE pass over the field.
+//
+// Replaces solver.py:82-113 (spatial_residual), numerics.py:90-196,
+// solver.py:116-125, solver.py:158-173 and, fused into the last stage,
+// solver.py:128-149 + 231-242.
+//
+// Work decomposition (B200):
+//  * The slowest axis (y in 2D, z in 3D) is MARCHED: a block owns a strip of
+//    NT (x) [x NTY (y, 3D)] columns and walks H rows along the march axis.
+//    Each thread keeps a 3-row register window of its column, so the
+//    march-axis faces and fluxes are computed exactly once per cell and each
+//    cell of u^s is read from HBM once per stage.
+//  * The in-plane axes (x; x and y in 3D) go through shared memory one row
+//    at a time.  Thread <-> "face cell" mapping: NT threads cover NT-2
+//    updated cells plus one halo face cell each side, so every WENO face pair
+//    is computed once per row and each interface flux once (+2/NT halo).
+//  * Ghost cells are never materialised for periodic/outflow axes: indices
+//    outside the interior are wrapped/clamped on load, which reproduces
+//    fill_boundary (grid.py:147-175) exactly; FVB_BC_HALO axes read ghosts
+//    from memory (filled by the halo exchange).
+//  * The transverse-interior crop of solver.py:99-104 means no corner ghost
+//    is ever read, so a face-only halo exchange is result-identical.
+//
+// This header is compiled twice (FVB_FAST=0 with -fmad=false -> namespace
+// exact; FVB_FAST=1 -> namespace fast).
+#pragma once
+#include <cuda_runtime.h>
+#include "fvb_physics.cuh"
+#include "fvb_state.cuh"
+
+namespace fvb {
+namespace FVB_NS {
+
+__device__ __forceinline__ int64_t map_index(int64_t i, int64_t n, int bc, int g) {
+  i = i < -g ? -g : (i > n + g - 1 ? n + g - 1 : i);   // memory safety
+  if (bc == FVB_BC_PERIODIC) return i < 0 ? i + n : (i >= n ? i - n : i);
+  if (bc == FVB_BC_OUTFLOW) return i < 0 ? 0 : (i >= n ? n - 1 : i);
+  return i;
+}
+
+template <int DIM>
+__device__ __forceinline__ int64_t cell_off(const StageParams& p, int64_t x, int64_t y, int64_t z) {
+  int64_t o = map_index(x, p.n[0], p.bc[0], p.g);
+  if (DIM >= 2) o += map_index(y, p.n[1], p.bc[1], p.g) * p.sy;
+  if (DIM >= 3) o += map_index(z, p.n[2], p.bc[2], p.g) * p.sz;
+  return o;
+}
+
+template <int NC>
+__device__ __forceinline__ void load_nc(const double* __restrict__ b, int64_t off, int64_t sc, double* v) {
+#pragma unroll
+  for (int c = 0; c < NC; ++c) v[c] = __ldg(b + off + c * sc);
+}
+
+__device__ __forceinline__ double ddiv(double a, const StageParams& p, int axis) {
+#if FVB_FAST
+  return a * p.id[axis];
+#else
+  return p.divd[axis] ? a / p.dd[axis] : a * p.id[axis];
+#endif
+}
+
+// RK stage combination (solver.py:166-173)
+__device__ __forceinline__ double rk_combine(int kind, double un, double us, double dt, double L) {
+#if FVB_FAST
+  switch (kind) {
+    case 0: return L;
+    case 1: return fma(dt, L, us);
+    case 2: return fma(0.5, un, 0.5 * fma(dt, L, us));
+    case 3: return fma(0.75, un, 0.25 * fma(dt, L, us));
+    default: return fma(1.0 / 3.0, un, (2.0 / 3.0) * fma(dt, L, us));
+  }
+#else
+  switch (kind) {
+    case 0: return L;
+    case 1: return us + dt * L;
+    case 2: return 0.5 * un + 0.5 * (us + dt * L);
+    case 3: return 0.75 * un + 0.25 * (us + dt * L);
+    default: return (1.0 / 3.0) * un + (2.0 / 3.0) * (us + dt * L);
+  }
+#endif
+}
+
+template <int DIM>
+__device__ __forceinline__ long long flat_cell(const StageParams& p, int64_t x, int64_t y, int64_t z) {
+  return ((long long)z * p.n[1] + y) * p.n[0] + x;
+}
+
+// Post-step work on the new value of one interior cell (last stage only).
+template <int EQ, int DIM, int NC>
+__device__ __forceinline__ void post_cell(const StageParams& p, FvbState* st, const double* v,
+                                          int64_t x, int64_t y, int64_t z, double* smax) {
+  const long long cell = flat_cell<DIM>(p, x, y, z);
+  const long long ncell = (long long)p.n[0] * p.n[1] * p.n[2];
+  bool finite = true;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    if (!isfinite(v[c])) {
+      if (finite) atomicMin(&st->bad_nonfinite, (long long)c * ncell + cell);
+      finite = false;
+    }
+  }
+  if constexpr (EQ == EQ_EULER) {
+    if (!euler_physical<DIM>(v, p.P)) atomicMin(&st->bad_unphys, cell);
+  }
+  double s[DIM];
+  wave_speeds<EQ, DIM>(v, p.P, s);
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) smax[k] = fmax(smax[k], s[k]);
+}
+
+// Block reduction of the per-thread maxima + last-block finalisation.
+template <int DIM>
+__device__ __forceinline__ void block_epilogue(const StageParams& p, FvbState* st, int inst,
+                                               const double* smax, bool post) {
+  const int lane = (threadIdx.y * blockDim.x + threadIdx.x) & 31;
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(smax[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned long long q = __shfl_xor_sync(0xffffffffu, b, o);
+      b = q > b ? q : b;
+    }
+    if (lane == 0 && b != 0ull) atomicMax(&st->smax[k], b);
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&st->blocks_done, 1u);
+    if (prev == p.nblocks - 1) {
+      __threadfence();
+      finalize_step(st, p.ctl, inst, post, true);
+    }
+  }
+}
+
+template <int DIM, int EQ, int FLUX, int RECON, int NT, int NTY>
+__global__ void __launch_bounds__(NT * NTY)
+stage_kernel(const StageParams p) {
+  constexpr int NC = NComp<EQ, DIM>::value;
+  constexpr bool WENO = RECON != RECON_NONE;
+  constexpr bool MARCH = DIM >= 2;
+  constexpr bool PY = DIM == 3;          // y handled in-plane (3D)
+  constexpr int SUY = PY ? NTY + 2 : 1;  // rows of the plane tile in smem
+  constexpr int OY = PY ? 1 : 0;
+  constexpr int MA = DIM - 1;            // march axis
+
+  // shared-memory carve-up (dynamic: the 3D Euler tile exceeds 48 KB)
+  extern __shared__ double smem[];
+  constexpr int nU = NC * SUY * (NT + 2);
+  constexpr int nFX = WENO ? NC * NTY * NT : 0;
+  constexpr int nGX = NC * NTY * NT;
+  constexpr int nFY = (WENO && PY) ? NC * NTY * NT : 0;
+  double* const pU = smem;
+  double* const pHx = pU + nU;
+  double* const pLx = pHx + nFX;
+  double* const pGx = pLx + nFX;
+  double* const pHy = pGx + nGX;
+  double* const pLy = pHy + nFY;
+  double* const pGy = pLy + nFY;
+#define sU(c, y, x) pU[((c) * SUY + (y)) * (NT + 2) + (x)]
+#define sHx(c, y, x) pHx[((c) * NTY + (y)) * NT + (x)]
+#define sLx(c, y, x) pLx[((c) * NTY + (y)) * NT + (x)]
+#define sGx(c, y, x) pGx[((c) * NTY + (y)) * NT + (x)]
+#define sHy(c, y, x) pHy[((c) * NTY + (y)) * NT + (x)]
+#define sLy(c, y, x) pLy[((c) * NTY + (y)) * NT + (x)]
+#define sGy(c, y, x) pGy[((c) * NTY + (y)) * NT + (x)]
+
+  const int tx = threadIdx.x;
+  const int ty = PY ? threadIdx.y : 0;
+  int inst, chunk;
+  int64_t y0 = 0;
+  if constexpr (DIM == 3) {
+    inst = blockIdx.z / p.chunks;
+    chunk = blockIdx.z % p.chunks;
+    y0 = (int64_t)blockIdx.y * (NTY - 2);
+  } else if constexpr (DIM == 2) {
+    inst = blockIdx.z;
+    chunk = blockIdx.y;
+  } else {
+    inst = blockIdx.z;
+    chunk = 0;
+  }
+  FvbState* st = p.st + inst;
+  if (*(volatile int*)&st->done) return;  // uniform over the block
+  const double dt = p.kind == 0 ? 0.0 : *(volatile double*)&st->dt;
+
+  const double* __restrict__ us = p.us + p.origin + inst * p.si;
+  const double* un = p.un + p.origin + inst * p.si;
+  double* out = p.out + p.origin + inst * p.si;
+
+  const int64_t nx = p.n[0], ny = p.n[1];
+  const int64_t x0 = (int64_t)blockIdx.x * (NT - 2);
+  const int64_t xf = x0 - 1 + tx;
+  const int64_t yf = PY ? y0 - 1 + ty : 0;
+  bool cell = tx >= 1 && tx <= NT - 2 && xf < nx;
+  if (PY) cell = cell && ty >= 1 && ty <= NTY - 2 && yf < ny;
+  const int64_t nm = MARCH ? p.n[MA] : 1;
+  const int64_t ra = MARCH ? (int64_t)chunk * p.H : 0;
+  const int64_t rb = MARCH ? min(ra + (int64_t)p.H, nm) : 1;
+
+  // march-axis coordinate helper: face cell of this thread at march row r
+  auto OFF = [&](int64_t x, int64_t y, int64_t r) -> int64_t {
+    if constexpr (DIM == 1) return cell_off<1>(p, x, 0, 0);
+    else if constexpr (DIM == 2) return cell_off<2>(p, x, r, 0);
+    else return cell_off<3>(p, x, y, r);
+  };
+
+  unsigned errb = 0;  // bit a: degenerate HLLC fan on axis a
+  double smax[DIM];
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) smax[k] = 0.0;
+
+  // register window of this thread's column: A = u[r-1], B = u[r], C = u[r+1]
+  double A[NC], B[NC], C[NC];
+  double hiP[NC], GP[NC], resP[NC], unP[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) { A[c] = B[c] = C[c] = hiP[c] = GP[c] = resP[c] = unP[c] = 0.0; }
+
+  int64_t rstart = MARCH ? ra - 1 : 0;
+  if constexpr (MARCH) {
+    load_nc<NC>(us, OFF(xf, yf, ra - 2), p.sc, A);
+    load_nc<NC>(us, OFF(xf, yf, ra - 1), p.sc, B);
+    load_nc<NC>(us, OFF(xf, yf, ra), p.sc, C);
+  } else {
+    load_nc<NC>(us, OFF(xf, yf, 0), p.sc, B);
+  }
+
+  for (int64_t r = rstart; r <= (MARCH ? rb : 0); ++r) {
+    double NX[NC], UNX[NC];
+    if constexpr (MARCH) {
+      if (r + 2 <= rb + 1) load_nc<NC>(us, OFF(xf, yf, r + 2), p.sc, NX);
+      if (p.kind >= 2 && cell && r >= ra && r < rb) {
+        const int64_t o = OFF(xf, yf, r);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) UNX[c] = un[o + c * p.sc];
+      }
+      // ---- march axis: faces of row r, flux (r-1 | r), finish row r-1 ----
+      if (cell) {
+        double hiC[NC], loC[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) weno_faces<RECON>(A[c], B[c], C[c], p.P.eps, hiC[c], loC[c]);
+        if (r >= ra) {
+          double uL[NC], uR[NC], G[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) { uL[c] = hiP[c]; uR[c] = loC[c]; }
+          fallback<EQ, DIM, RECON>(uL, uR, A, B, p.P);
+          unsigned eb = 0;
+          num_flux<EQ, FLUX, DIM>(uL, uR, MA, p.P, G, eb);
+          if (eb) errb |= 1u << MA;
+          if (r - 1 >= ra) {
+            double v[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+#if FVB_FAST
+              const double Lc = fma(GP[c] - G[c], p.id[MA], resP[c]);
+#else
+              const double Lc = resP[c] - ddiv(G[c] - GP[c], p, MA);
+#endif
+              v[c] = rk_combine(p.kind, unP[c], A[c], dt, Lc);
+            }
+            const int64_t o = OFF(xf, yf, r - 1);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
+            if (p.final_stage) post_cell<EQ, DIM, NC>(p, st, v, xf, yf, r - 1, smax);
+          }
+#pragma unroll
+          for (int c = 0; c < NC; ++c) GP[c] = G[c];
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) hiP[c] = hiC[c];
+      }
+    }
+
+    // ---- in-plane axes for row r ----
+    if (r >= ra && r < rb) {
+      // stage-start interior check (solver.py:90-93)
+      if constexpr (EQ == EQ_EULER) {
+        if (cell && !euler_physical<DIM>(B, p.P)) {
+          const long long key = ((long long)p.stage_idx << 42) | flat_cell<DIM>(p, xf, yf, MARCH ? r : 0);
+          atomicMin(&st->stage_err, key);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) sU(c, ty + OY, tx + 1) = B[c];
+      if constexpr (WENO) {
+        if ((!PY || (ty >= 1 && ty <= NTY - 2)) && (tx == 0 || tx == NT - 1)) {
+          const int64_t hxo = OFF(tx == 0 ? x0 - 2 : x0 + NT - 1, yf, r);
+          const int col = tx == 0 ? 0 : NT + 1;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) sU(c, ty + OY, col) = __ldg(us + hxo + c * p.sc);
+        }
+        if constexpr (PY) {
+          if ((ty == 0 || ty == NTY - 1) && tx >= 1 && tx <= NT - 2) {
+            const int64_t hyo = OFF(xf, ty == 0 ? y0 - 2 : y0 + NTY - 1, r);
+            const int row = ty == 0 ? 0 : NTY + 1;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) sU(c, row, tx + 1) = __ldg(us + hyo + c * p.sc);
+          }
+        }
+      }
+      __syncthreads();
+      if constexpr (WENO) {
+        if (!PY || (ty >= 1 && ty <= NTY - 2)) {
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+            weno_faces<RECON>(sU(c, ty + OY, tx), sU(c, ty + OY, tx + 1), sU(c, ty + OY, tx + 2), p.P.eps,
+                              sHx(c, ty, tx), sLx(c, ty, tx));
+        }
+        if constexpr (PY) {
+          if (tx >= 1 && tx <= NT - 2) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+              weno_faces<RECON>(sU(c, ty, tx + 1), sU(c, ty + 1, tx + 1), sU(c, ty + 2, tx + 1), p.P.eps,
+                                sHy(c, ty, tx), sLy(c, ty, tx));
+          }
+        }
+        __syncthreads();
+      }
+      // interface fluxes: x interface tx sits between face cells tx-1 and tx
+      if (tx >= 1 && (!PY || (ty >= 1 && ty <= NTY - 2))) {
+        double uL[NC], uR[NC], cl[NC], cr[NC], G[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          cl[c] = sU(c, ty + OY, tx);
+          cr[c] = sU(c, ty + OY, tx + 1);
+          if constexpr (WENO) {
+            uL[c] = sHx(c, ty, tx - 1);
+            uR[c] = sLx(c, ty, tx);
+          } else {
+            uL[c] = cl[c];
+            uR[c] = cr[c];
+          }
+        }
+        fallback<EQ, DIM, RECON>(uL, uR, cl, cr, p.P);
+        unsigned eb = 0;
+        num_flux<EQ, FLUX, DIM>(uL, uR, 0, p.P, G, eb);
+        if (eb && xf <= nx && (!PY || yf < ny)) errb |= 1u;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) sGx(c, ty, tx) = G[c];
+      }
+      if constexpr (PY) {
+        if (ty >= 1 && tx >= 1 && tx <= NT - 2) {
+          double uL[NC], uR[NC], cl[NC], cr[NC], G[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            cl[c] = sU(c, ty, tx + 1);
+            cr[c] = sU(c, ty + 1, tx + 1);
+            if constexpr (WENO) {
+              uL[c] = sHy(c, ty - 1, tx);
+              uR[c] = sLy(c, ty, tx);
+            } else {
+              uL[c] = cl[c];
+              uR[c] = cr[c];
+            }
+          }
+          fallback<EQ, DIM, RECON>(uL, uR, cl, cr, p.P);
+          unsigned eb = 0;
+          num_flux<EQ, FLUX, DIM>(uL, uR, 1, p.P, G, eb);
+          if (eb && yf <= ny && xf < nx) errb |= 2u;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) sGy(c, ty, tx) = G[c];
+        }
+      }
+      __syncthreads();
+      if (cell) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+#if FVB_FAST
+          double res = (sGx(c, ty, tx) - sGx(c, ty, tx + 1)) * p.id[0];
+          if constexpr (PY) res = fma(sGy(c, ty, tx) - sGy(c, ty + 1, tx), p.id[1], res);
+#else
+          double res = 0.0 - ddiv(sGx(c, ty, tx + 1) - sGx(c, ty, tx), p, 0);
+          if constexpr (PY) res = res - ddiv(sGy(c, ty + 1, tx) - sGy(c, ty, tx), p, 1);
+#endif
+          resP[c] = res;
+        }
+        if constexpr (!MARCH) {
+          // 1D: the in-plane residual is the whole residual
+          double v[NC];
+          const int64_t o = OFF(xf, 0, 0);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const double unc = p.kind >= 2 ? un[o + c * p.sc] : 0.0;
+            v[c] = rk_combine(p.kind, unc, B[c], dt, resP[c]);
+          }
+#pragma unroll
+          for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
+          if (p.final_stage) post_cell<EQ, DIM, NC>(p, st, v, xf, 0, 0, smax);
+        }
+      }
+    }
+    if constexpr (MARCH) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        A[c] = B[c];
+        B[c] = C[c];
+        C[c] = NX[c];
+        unP[c] = UNX[c];
+      }
+    }
+  }
+
+  if (errb) {
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+      if (errb & (1u << a))
+        atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | ((long long)(1 + a) << 40));
+  }
+  if (p.final_stage) block_epilogue<DIM>(p, st, inst, smax, true);
+#undef sU
+#undef sHx
+#undef sLx
+#undef sGx
+#undef sHy
+#undef sLy
+#undef sGy
+}
+
+template <int DIM, int EQ, int RECON, int NT, int NTY>
+constexpr int stage_smem_bytes() {
+  constexpr int NC = NComp<EQ, DIM>::value;
+  constexpr bool WENO = RECON != RECON_NONE;
+  constexpr bool PY = DIM == 3;
+  constexpr int SUY = PY ? NTY + 2 : 1;
+  return 8 * (NC * SUY * (NT + 2) + (WENO ? 2 : 0) * NC * NTY * NT + NC * NTY * NT +
+              ((WENO && PY) ? 2 : 0) * NC * NTY * NT + (PY ? NC * NTY * NT : 0));
+}
+
+// Standalone wave-speed pass: solver.py:128-136 (+ the initial is_physical
+// check of solver.py:211-212).  finalize = 1 also computes the first dt.
+template <int DIM, int EQ>
+__global__ void __launch_bounds__(256) speed_kernel(const StageParams p, int finalize) {
+  constexpr int NC = NComp<EQ, DIM>::value;
+  const int inst = blockIdx.y;
+  FvbState* st = p.st + inst;
+  const double* u = p.us + p.origin + inst * p.si;
+  double smax[DIM];
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) smax[k] = 0.0;
+  const int64_t ncell = p.n[0] * p.n[1] * p.n[2];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncell;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = i % p.n[0];
+    const int64_t yz = i / p.n[0];
+    const int64_t y = yz % p.n[1];
+    const int64_t z = yz / p.n[1];
+    const int64_t o = x + y * p.sy + z * p.sz;
+    double v[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) v[c] = u[o + c * p.sc];
+    if constexpr (EQ == EQ_EULER) {
+      if (!euler_physical<DIM>(v, p.P)) atomicMin(&st->bad_unphys, (long long)i);
+    }
+    double s[DIM];
+    wave_speeds<EQ, DIM>(v, p.P, s);
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) smax[k] = fmax(smax[k], s[k]);
+  }
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(smax[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned long long q = __shfl_xor_sync(0xffffffffu, b, o);
+      b = q > b ? q : b;
+    }
+    if (lane == 0 && b != 0ull) atomicMax(&st->smax[k], b);
+  }
+  if (!finalize) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&st->blocks_done, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence();
+      finalize_step(st, p.ctl, inst, false, true);
+    }
+  }
+}
+
+// host-side launchers (defined in fvb_kernels.cu, once per namespace)
+int launch_stage(int dim, int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s);
+int launch_speed(int dim, int eq, const StageParams& p, int finalize, dim3 grid, cudaStream_t s);
+void stage_block(int dim, int& nt, int& nty);
+
+}  // namespace FVB_NS
+}  // namespace fvb

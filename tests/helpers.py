@@ -18,3 +18,18 @@ def rel_l1(a, b):
     b = np.asarray(b, dtype=float)
     den = np.abs(b).sum()
     return float(np.abs(a - b).sum() / den) if den else float(np.abs(a - b).sum())
+
+
+def product_objects(d: dict):
+    """(GridSpec, SchemeConfig) of the B200 package from a golden scheme dict."""
+    import paper_1912_07645_b200 as P
+
+    dim = d["dim"]
+    grid = P.GridSpec(dim, tuple(d["cells"]), (0.0,) * dim,
+                      tuple(c * dl for c, dl in zip(d["cells"], d["deltas"])),
+                      ghost_width=d["ghost"], deltas=tuple(d["deltas"]))
+    model = P.EquationModel(d["eq"], dim, gamma=d["gamma"], advection_speed=tuple(d["adv"]))
+    cfg = P.SchemeConfig(model, P.FluxKind(d["flux"]), P.Reconstruction(P.ReconstructionKind(d["recon"]), d["eps"]),
+                         rk_order=d["rk"], cfl=d["cfl"], t_end=d["t_end"],
+                         bc=tuple(P.BoundaryKind(b) for b in d["bcs"]))
+    return grid, cfg

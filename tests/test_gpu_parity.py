@@ -1,0 +1,165 @@
+"""GPU parity: the CUDA path (through the C ABI) against the golden fixtures
+generated from the reference, and against the CPU oracle on the same inputs.
+
+Exact arithmetic must be BITWISE equal (SHA of the interior bytes); fast
+arithmetic must stay within relative L1 <= 1e-12 per component over the
+same windows (north-star tolerance)."""
+import numpy as np
+import pytest
+
+from oracle import fv_oracle as O
+from tests.helpers import oracle_scheme, product_objects, rel_l1
+
+pytestmark = pytest.mark.gpu
+
+TOL_FAST = 1e-12
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1912_07645_b200 as P
+
+    return P
+
+
+def _init_field(P, case, arrays, grid):
+    key = case["name"] + "__init"
+    if key in arrays:
+        data = np.array(arrays[key])
+    else:
+        sc = oracle_scheme(case["scheme"])
+        data = O.kelvin_helmholtz(tuple(sc.cells), case["vector"], ghost=sc.ghost)
+    return P.Field(grid, data.shape[0], data)
+
+
+@pytest.mark.parametrize("idx", range(47))
+def test_run_simulation_exact_bitwise(P, golden, golden_arrays, idx):
+    runs = golden["runs"]
+    if idx >= len(runs):
+        pytest.skip("no such case")
+    case = runs[idx]
+    grid, cfg = product_objects(case["scheme"])
+    init = _init_field(P, case, golden_arrays, grid)
+    assert O.sha16(init.interior) == case["init_sha"]
+    final, recs = P.run_simulation(init, cfg, max_steps=case["max_steps"], arith="exact")
+    assert len(recs) == case["steps"], case["name"]
+    assert [r.dt for r in recs[:8]] == case["dts"], case["name"]
+    assert O.sha16(np.array([r.dt for r in recs])) == case["dt_sha"], case["name"]
+    assert recs[-1].t == case["t"]
+    assert O.sha16(final.interior) == case["final_sha"], case["name"]
+    assert O.sha16(final.data) == case["data_sha"], case["name"]
+
+
+@pytest.mark.parametrize("name", ["kh2d64_weno2_50", "kh2d32_weno3_20", "kh3d16_weno2_5", "euler2d_hllc_weno3_outflow",
+                                  "euler3d_rusanov_weno2_outflow", "burgers2d64_qmc0", "double_rarefaction",
+                                  "sod400_preset", "advection2d_weno3_rk3"])
+def test_run_simulation_fast_tolerance(P, golden, golden_arrays, name):
+    case = next(r for r in golden["runs"] if r["name"] == name)
+    grid, cfg = product_objects(case["scheme"])
+    init = _init_field(P, case, golden_arrays, grid)
+    final, recs = P.run_simulation(init, cfg, max_steps=case["max_steps"], arith="fast")
+    ref = golden_arrays[name + "__final"]
+    sc = oracle_scheme(case["scheme"])
+    ref_in = O.interior(ref, sc)
+    assert abs(len(recs) - case["steps"]) <= 1
+    n = min(len(recs), case["steps"])
+    for c in range(ref_in.shape[0]):
+        if len(recs) == case["steps"]:
+            assert rel_l1(final.interior[c], ref_in[c]) <= TOL_FAST, (name, c)
+
+
+def test_residual_and_maxima_bitwise(P, golden, golden_arrays):
+    for case in golden["residuals"]:
+        grid, cfg = product_objects(case["scheme"])
+        u = np.array(golden_arrays[case["name"] + "__u"])
+        f = P.Field(grid, u.shape[0], u)
+        L = P.spatial_residual(f, cfg, arith="exact")
+        assert O.sha16(L) == case["L_sha"], case["name"]
+        mx = P.wave_speed_maxima(f, cfg)
+        assert list(mx) == case["max"], case["name"]
+
+
+def test_residual_fast_close(P, golden, golden_arrays):
+    for case in golden["residuals"]:
+        grid, cfg = product_objects(case["scheme"])
+        u = np.array(golden_arrays[case["name"] + "__u"])
+        L = P.spatial_residual(P.Field(grid, u.shape[0], u), cfg, arith="fast")
+        ref = golden_arrays[case["name"] + "__L"]
+        for c in range(ref.shape[0]):
+            assert rel_l1(L[c], ref[c]) <= 1e-13, (case["name"], c)
+
+
+def test_fill_boundary_matches_oracle(P, golden, golden_arrays):
+    for case in golden["residuals"][:24]:
+        grid, cfg = product_objects(case["scheme"])
+        sc = oracle_scheme(case["scheme"])
+        u = np.array(golden_arrays[case["name"] + "__u"])
+        raw = O.padded_from_interior(sc, O.interior(u, sc))
+        f = P.Field(grid, raw.shape[0], raw.copy())
+        P.fill_boundary(f, cfg.bc)
+        assert O.sha16(f.data) == case["filled_sha"], case["name"]
+
+
+def test_ssp_rk_step_bitwise(P, golden, golden_arrays):
+    for case in golden["residuals"][::5]:
+        grid, cfg = product_objects(case["scheme"])
+        sc = oracle_scheme(case["scheme"])
+        u = np.array(golden_arrays[case["name"] + "__u"])
+        for rk in (1, 2, 3):
+            sc.rk = rk
+            cfg2 = P.SchemeConfig(cfg.model, cfg.flux, cfg.recon, rk, cfg.cfl, cfg.t_end, cfg.bc)
+            dt = 1e-3
+            ref = O.step(u, dt, sc)
+            out = P.ssp_rk_step(P.Field(grid, u.shape[0], u.copy()), dt, cfg2)
+            assert O.sha16(out.data) == O.sha16(ref), (case["name"], rk)
+
+
+def test_error_cases(P, golden):
+    errs = {e["name"]: e for e in golden["errors"]}
+    grid = P.GridSpec(1, (8,), (0.0,), (1.0,), ghost_width=1)
+    cfg = P.SchemeConfig(P.EquationModel("euler", 1), P.FluxKind.HLLC, P.Reconstruction(), rk_order=1, t_end=0.1,
+                         bc=(P.BoundaryKind.PERIODIC,))
+    u = np.zeros((3, 8))
+    u[0] = 1.0
+    u[2] = 2.5
+    u[0, 5] = -1.0
+    with pytest.raises(P.SimulationError) as ei:
+        P.run_simulation(P.field_from_interior(grid, u), cfg)
+    assert str(ei.value) == errs["unphysical_init"]["msg"]
+    grid = P.GridSpec(2, (6, 5), (0.0, 0.0), (1.0, 1.0), ghost_width=2)
+    cfg = P.SchemeConfig(P.EquationModel("burgers", 2), P.FluxKind.RUSANOV,
+                         P.Reconstruction(P.ReconstructionKind.WENO2), rk_order=3, t_end=0.1)
+    with pytest.raises(P.StaticFieldError) as ei:
+        P.run_simulation(P.field_from_interior(grid, np.zeros((1, 5, 6))), cfg)
+    assert str(ei.value) == errs["static_field"]["msg"]
+    grid = P.GridSpec(1, (16,), (0.0,), (1.0,), ghost_width=1)
+    cfg = P.SchemeConfig(P.EquationModel("burgers", 1), P.FluxKind.RUSANOV, P.Reconstruction(), rk_order=1,
+                         t_end=1.0)
+    u = np.ones((1, 16))
+    u[0, 9] = 1e200
+    with pytest.raises(P.SimulationError) as ei:
+        P.run_simulation(P.field_from_interior(grid, u), cfg)
+    assert str(ei.value) == errs["nonfinite"]["msg"]
+
+
+def test_observers_sequence(P, golden, golden_arrays):
+    case = next(r for r in golden["runs"] if r["name"] == "burgers1d_weno3_rk3_outflow")
+    grid, cfg = product_objects(case["scheme"])
+    init = _init_field(P, case, golden_arrays, grid)
+    seen = []
+    final, recs = P.run_simulation(init, cfg, observers=[lambda s, t, f: seen.append((s, t, O.sha16(f.interior)))],
+                                   max_steps=12)
+    assert [s for s, _, _ in seen] == list(range(13))
+    assert seen[0][1] == 0.0 and seen[0][2] == case["init_sha"]
+    assert [t for _, t, _ in seen[1:]] == [r.t for r in recs]
+    assert seen[-1][2] == O.sha16(final.interior)
+
+
+def test_device_field_roundtrip(P, golden, golden_arrays):
+    case = next(r for r in golden["runs"] if r["name"] == "kh2d64_weno2_50")
+    grid, cfg = product_objects(case["scheme"])
+    init = _init_field(P, case, golden_arrays, grid)
+    dev = P.DeviceField.from_host(init)
+    out, recs = P.run_simulation(dev, cfg, max_steps=50)
+    assert isinstance(out, P.DeviceField)
+    assert O.sha16(out.interior.cpu().numpy()) == case["final_sha"]
