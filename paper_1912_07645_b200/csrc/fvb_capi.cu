@@ -61,7 +61,9 @@ struct RunPlan {
 
 struct fvb_ctx {
   int device;
-  cudaStream_t stream;
+  cudaStream_t stream;      // stream all work is issued on
+  cudaStream_t own_stream;  // created when the caller passes the legacy NULL stream
+
   char msg[1024];
   FvbState* d_state;  // run state, one per instance
   int state_cap;
@@ -269,12 +271,20 @@ int fvb_ctx_create(int device, void* stream, fvb_ctx** out) {
   fvb_ctx* ctx = new fvb_ctx;
   std::memset(ctx, 0, sizeof(*ctx));
   ctx->device = device;
-  ctx->stream = (cudaStream_t)stream;
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) {
     *out = ctx;
     return set_err(ctx, FVB_E_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
   }
+  // CUDA graphs cannot be captured on the legacy NULL stream.  A blocking
+  // stream created here is implicitly ordered with NULL-stream work (torch's
+  // default stream), so callers see ordinary stream semantics.
+  e = cudaStreamCreate(&ctx->own_stream);
+  if (e != cudaSuccess) {
+    *out = ctx;
+    return set_err(ctx, FVB_E_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+  }
+  ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
   e = cudaMalloc(&ctx->d_scratch_state, sizeof(FvbState) * 4096);
   if (e != cudaSuccess) {
     *out = ctx;
@@ -291,13 +301,15 @@ int fvb_ctx_destroy(fvb_ctx* ctx) {
   if (ctx->d_scratch_state) cudaFree(ctx->d_scratch_state);
   if (ctx->d_log) cudaFree(ctx->d_log);
   if (ctx->d_partials) cudaFree(ctx->d_partials);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return FVB_OK;
 }
 
 int fvb_ctx_set_stream(fvb_ctx* ctx, void* stream) {
-  if (ctx->stream != (cudaStream_t)stream) destroy_graph(ctx);
-  ctx->stream = (cudaStream_t)stream;
+  cudaStream_t s = stream ? (cudaStream_t)stream : ctx->own_stream;
+  if (ctx->stream != s) destroy_graph(ctx);
+  ctx->stream = s;
   return FVB_OK;
 }
 
