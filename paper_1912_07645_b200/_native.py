@@ -14,7 +14,7 @@ from pathlib import Path
 
 from . import errors as E
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libfvb200.so"
+LIB_PATH = Path(os.environ.get("FVB_LIB") or Path(__file__).resolve().parent / "_lib" / "libfvb200.so")
 
 # status codes (fvb200.h)
 OK, E_CONFIG, E_UNPHYSICAL, E_SIMULATION, E_STATIC, E_PROTOCOL, E_CUDA = range(7)

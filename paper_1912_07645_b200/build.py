@@ -40,32 +40,44 @@ def _sources_digest() -> str:
     return h.hexdigest()
 
 
-def _compile(unit):
+def _compile(unit, out: Path = OUT):
     src, obj, flags = unit
-    cmd = [NVCC] + COMMON + flags + ["-c", str(CSRC / src), "-o", str(OUT / obj)]
+    cmd = [NVCC] + COMMON + flags + ["-c", str(CSRC / src), "-o", str(out / obj)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
     return obj
 
 
-def build(force: bool = False, verbose: bool = True) -> Path:
-    OUT.mkdir(exist_ok=True)
-    stamp = OUT / "build.sha256"
-    digest = _sources_digest()
-    if LIB.exists() and stamp.exists() and stamp.read_text() == digest and not force:
-        return LIB
-    with cf.ThreadPoolExecutor(max_workers=len(UNITS)) as ex:
-        list(ex.map(_compile, UNITS))
-    cmd = [NVCC] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", str(LIB)] + [str(OUT / u[1]) for u in UNITS]
+def build(force: bool = False, verbose: bool = True, extra=(), out_dir: Path | None = None) -> Path:
+    """Compile the four translation units and link libfvb200.so.  ``extra``
+    adds nvcc flags (tuning experiments build variants into ``out_dir``)."""
+    out = Path(out_dir) if out_dir else OUT
+    out.mkdir(parents=True, exist_ok=True)
+    lib = out / "libfvb200.so"
+    stamp = out / "build.sha256"
+    digest = _sources_digest() + "|" + " ".join(extra)
+    if lib.exists() and stamp.exists() and stamp.read_text() == digest and not force:
+        return lib
+    units = [(src, obj, flags + list(extra)) for src, obj, flags in UNITS]
+    with cf.ThreadPoolExecutor(max_workers=len(units)) as ex:
+        list(ex.map(lambda u: _compile(u, out), units))
+    cmd = [NVCC] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", str(lib)] + [str(out / u[1]) for u in UNITS]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     stamp.write_text(digest)
     if verbose:
-        print(f"built {LIB}", file=sys.stderr)
-    return LIB
+        print(f"built {lib}", file=sys.stderr)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--out", default=None)
+    ap.add_argument("extra", nargs="*", help="extra nvcc flags, e.g. -DFVB_STRIP_MINB=3")
+    a = ap.parse_args()
+    build(force=a.force, extra=a.extra, out_dir=a.out)

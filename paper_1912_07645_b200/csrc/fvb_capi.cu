@@ -20,12 +20,12 @@ namespace fvb {
 namespace exact {
 int launch_stage(int dim, int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s);
 int launch_speed(int dim, int eq, const StageParams& p, int finalize, dim3 grid, cudaStream_t s);
-void stage_block(int dim, int& nt, int& nty);
+void stage_block(int dim, int variant, int& nt, int& nty);
 }  // namespace exact
 namespace fast {
 int launch_stage(int dim, int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s);
 int launch_speed(int dim, int eq, const StageParams& p, int finalize, dim3 grid, cudaStream_t s);
-void stage_block(int dim, int& nt, int& nty);
+void stage_block(int dim, int variant, int& nt, int& nty);
 }  // namespace fast
 // fvb_aux.cu
 int launch_fill_axis(const fvb_scheme& s, const fvb_layout& L, double* u, int ninst, int axis, cudaStream_t st);
@@ -162,8 +162,12 @@ static StageParams base_params(const fvb_scheme& s, const fvb_layout& L) {
 // Grid of the stage kernel; fills chunks / H / nblocks.
 static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst) {
   int nt, nty;
-  if (s.arith == FVB_ARITH_FAST) fvb::fast::stage_block(s.dim, nt, nty);
-  else fvb::exact::stage_block(s.dim, nt, nty);
+  const char* kv = getenv("FVB_KERNEL");
+  // 2D default: shared-memory tile kernel (fastest measured);
+  // FVB_KERNEL=strip selects the warp-strip kernel
+  p.variant = (kv && std::strcmp(kv, "strip") == 0) ? 0 : 1;
+  if (s.arith == FVB_ARITH_FAST) fvb::fast::stage_block(s.dim, p.variant, nt, nty);
+  else fvb::exact::stage_block(s.dim, p.variant, nt, nty);
   const int64_t strips = (p.n[0] + (nt - 2) - 1) / (nt - 2);
   dim3 g(1, 1, 1);
   g.x = (unsigned)strips;
@@ -173,7 +177,7 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst) {
     int64_t ytiles = 1;
     if (s.dim == 3) ytiles = (p.n[1] + (nty - 2) - 1) / (nty - 2);
     // aim for ~2 waves of resident blocks over 148 SMs
-    const int64_t per_sm = s.dim == 3 ? 1 : 6;
+    const int64_t per_sm = s.dim == 3 ? 1 : (p.variant == 0 ? 4 : 6);
     const int64_t target = 148 * per_sm * 2;
     int64_t want_chunks = (target + strips * ytiles * ninst - 1) / (strips * ytiles * ninst);
     want_chunks = std::max<int64_t>(1, std::min<int64_t>(want_chunks, nm));

@@ -6,19 +6,28 @@
 namespace fvb {
 namespace FVB_NS {
 
+// 3D: smem tile kernel (NT x NTY face cells); 1D/2D: warp-strip kernel
+// (variant 0) or the smem tile kernel marching in y (variant 1)
 template <int DIM> struct Blk;
 template <> struct Blk<1> { static constexpr int NT = 128, NTY = 1; };
 template <> struct Blk<2> { static constexpr int NT = 64, NTY = 1; };
 template <> struct Blk<3> { static constexpr int NT = 32, NTY = 8; };
+constexpr int kStripWarps = 4;
 
-void stage_block(int dim, int& nt, int& nty) {
-  if (dim == 1) { nt = Blk<1>::NT; nty = Blk<1>::NTY; }
-  else if (dim == 2) { nt = Blk<2>::NT; nty = Blk<2>::NTY; }
+// cells per block along x (reported as nt-2) and the y tile (nty-2, 3D only)
+void stage_block(int dim, int variant, int& nt, int& nty) {
+  if (dim <= 2 && variant == 0) { nt = kStripCells * kStripWarps + 2; nty = 1; }
+  else if (dim == 1) { nt = Blk<1>::NT; nty = 1; }
+  else if (dim == 2) { nt = Blk<2>::NT; nty = 1; }
   else { nt = Blk<3>::NT; nty = Blk<3>::NTY; }
 }
 
 template <int DIM, int EQ, int FLUX, int RECON>
 static int launch_one(const StageParams& p, dim3 grid, cudaStream_t s) {
+  if (DIM <= 2 && p.variant == 0) {
+    strip_kernel<DIM, EQ, FLUX, RECON, kStripWarps><<<grid, 32 * kStripWarps, 0, s>>>(p);
+    return 0;
+  } else {
   constexpr int NT = Blk<DIM>::NT, NTY = Blk<DIM>::NTY;
   constexpr int smem = stage_smem_bytes<DIM, EQ, RECON, NT, NTY>();
   auto kern = stage_kernel<DIM, EQ, FLUX, RECON, NT, NTY>;
@@ -30,6 +39,7 @@ static int launch_one(const StageParams& p, dim3 grid, cudaStream_t s) {
   }
   kern<<<grid, dim3(NT, NTY), smem, s>>>(p);
   return 0;
+  }
 }
 
 template <int DIM>

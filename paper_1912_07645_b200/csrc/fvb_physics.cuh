@@ -8,8 +8,9 @@
 //                  identical to numpy (one IEEE binary64 op per numpy pass).
 //   FVB_FAST == 1  "fast": same algorithm, algebraically restructured to
 //                  remove divides (one reciprocal per WENO pair, 1/rho per
-//                  state) and FMA-contracted; parity is relative L1 <= 1e-12
-//                  over the test windows.
+//                  state, MUFU reciprocal/rsqrt seeds + Newton steps) and
+//                  FMA-contracted; parity is relative L1 <= 1e-12 over the
+//                  test windows (tests/test_gpu_parity.py).
 //
 // Reference citations: /root/reference/pkg/src/conslaw/<file>:<line>.
 #pragma once
@@ -27,6 +28,34 @@ namespace fvb {
 __device__ __forceinline__ double np_max(double a, double b) { return (a > b || a != a) ? a : b; }
 __device__ __forceinline__ double np_min(double a, double b) { return (a < b || a != a) ? a : b; }
 
+#if FVB_FAST
+// 1/x: MUFU seed + two Newton steps (full double precision for normal x)
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+// a/b with one residual correction
+__device__ __forceinline__ double fdiv(double a, double b) {
+  const double r = frcp(b);
+  const double q = a * r;
+  return fma(fma(-b, q, a), r, q);
+}
+// sqrt(x), x > 0: rsqrt seed + Newton, final residual correction
+__device__ __forceinline__ double fsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  double s = x * y;
+  return fma(fma(-s, s, x), 0.5 * y, s);  // x > 0 on every physical state
+}
+#endif
+
 // ---------------------------------------------------------------------------
 // Euler equation of state (equations.py:62-73, 128-129)
 // ---------------------------------------------------------------------------
@@ -37,7 +66,7 @@ __device__ __forceinline__ double euler_pressure(const double* u, const Phys& P)
 #pragma unroll
   for (int k = 1; k < DIM; ++k) msq = msq + u[1 + k] * u[1 + k];
 #if FVB_FAST
-  return P.gm1 * (u[1 + DIM] - msq * (0.5 / u[0]));
+  return P.gm1 * (u[1 + DIM] - msq * (0.5 * frcp(u[0])));
 #else
   return P.gm1 * (u[1 + DIM] - msq / (2.0 * u[0]));
 #endif
@@ -48,7 +77,7 @@ __device__ __forceinline__ bool euler_physical(const double* u, const Phys& P) {
   return (u[0] > kFloor) & (euler_pressure<DIM>(u, P) > kFloor);
 }
 
-// Physical flux F_axis(u) (equations.py:91-110), given p.
+// Physical flux F_axis(u) (equations.py:91-110), given p and v = m_axis/rho.
 template <int DIM>
 __device__ __forceinline__ void euler_flux(const double* u, double p, double v, int axis, double* f) {
   f[0] = u[1 + axis];
@@ -59,21 +88,23 @@ __device__ __forceinline__ void euler_flux(const double* u, double p, double v, 
 }
 
 // Per-state quantities shared by flux, wave speed and HLLC.
-struct EState { double rho, v, p, c; };
+struct EState { double rho, v, p, c, rinv; };
 
 template <int DIM>
 __device__ __forceinline__ EState euler_state(const double* u, int axis, const Phys& P) {
   EState s;
   s.rho = u[0];
 #if FVB_FAST
-  const double r = 1.0 / u[0];
+  const double r = frcp(u[0]);
+  s.rinv = r;
   s.v = u[1 + axis] * r;
   double msq = u[1] * u[1];
 #pragma unroll
   for (int k = 1; k < DIM; ++k) msq = fma(u[1 + k], u[1 + k], msq);
-  s.p = P.gm1 * (u[1 + DIM] - 0.5 * msq * r);
-  s.c = sqrt(P.gamma * s.p * r);
+  s.p = P.gm1 * fma(-0.5 * msq, r, u[1 + DIM]);
+  s.c = fsqrt(P.gamma * s.p * r);
 #else
+  s.rinv = 0.0;
   s.v = u[1 + axis] / s.rho;                      // numerics.py:159
   s.p = euler_pressure<DIM>(u, P);                // numerics.py:160
   s.c = sqrt(P.gamma * s.p / s.rho);              // equations.py:128-129
@@ -109,14 +140,14 @@ __device__ __forceinline__ void weno_faces(double um, double uc, double up, doub
     const double q1 = e1 * e1;
     if constexpr (RECON == RECON_WENO2) {
       // w0 = q1/(q0+q1), w1 = q0/(q0+q1)
-      const double h = (0.5 / (q0 + q1)) * fma(q1, D0, q0 * D1);
+      const double h = (0.5 * frcp(q0 + q1)) * fma(q1, D0, q0 * D1);
       hi = uc + h;
       lo = uc - h;
     } else {
       // high face: a0 = (1/3)/q0, a1 = (2/3)/q1 -> w0 = q1/(q1 + 2 q0)
       // low face : a0 = (1/3)/q1, a1 = (2/3)/q0 -> w0' = q0/(q0 + 2 q1)
-      const double th = fma(q1, D0, 2.0 * q0 * D1) / fma(2.0, q0, q1);
-      const double tl = fma(q0, D1, 2.0 * q1 * D0) / fma(2.0, q1, q0);
+      const double th = fma(q1, D0, 2.0 * q0 * D1) * frcp(fma(2.0, q0, q1));
+      const double tl = fma(q0, D1, 2.0 * q1 * D0) * frcp(fma(2.0, q1, q0));
       hi = fma(0.5, th, uc);
       lo = fma(-0.5, tl, uc);
     }
@@ -151,17 +182,15 @@ __device__ __forceinline__ void weno_faces(double um, double uc, double up, doub
 }
 
 // ---------------------------------------------------------------------------
-// Numerical fluxes.  Error bit 1 = degenerate HLLC fan (numerics.py:166-167).
+// Numerical fluxes.  errbits |= 1: degenerate HLLC fan (numerics.py:166-167).
 // ---------------------------------------------------------------------------
 
 // Rusanov (numerics.py:133-142)
 template <int EQ, int DIM>
-__device__ __forceinline__ void rusanov(const double* uL, const double* uR, int axis,
-                                        const Phys& P, double* F) {
+__device__ __forceinline__ void rusanov(const double* uL, const double* uR, const EState& L, const EState& R,
+                                        int axis, const Phys& P, double* F) {
   constexpr int NC = NComp<EQ, DIM>::value;
   if constexpr (EQ == EQ_EULER) {
-    const EState L = euler_state<DIM>(uL, axis, P);
-    const EState R = euler_state<DIM>(uR, axis, P);
     double fL[NC], fR[NC];
     euler_flux<DIM>(uL, L.p, L.v, axis, fL);
     euler_flux<DIM>(uR, R.p, R.v, axis, fR);
@@ -183,95 +212,102 @@ __device__ __forceinline__ void rusanov(const double* uL, const double* uR, int 
   }
 }
 
-// HLLC with Davis speeds (numerics.py:145-196).  Only the selected branch of
-// the reference's nested np.where is evaluated; the selected value is the
-// same expression, so results are identical.
+// HLLC with Davis speeds (numerics.py:145-196), branch free: the side K of
+// the reference's nested np.where (sL>=0 -> fL; sM>=0 -> F*L; sR>0 -> F*R;
+// else fR; uL==uR -> fL) is selected first, then ONE physical flux and ONE
+// star state are evaluated for that side.  The selected value is the same
+// expression as the reference's, so the exact mode stays bitwise.  Work a
+// whole warp does not need is skipped on a warp vote (uniform regions, where
+// every lane has uL == uR, cost one physical flux).
 template <int DIM>
-__device__ __forceinline__ void hllc(const double* uL, const double* uR, int axis,
-                                     const Phys& P, double* F, unsigned& errbits) {
+__device__ __forceinline__ void hllc(const double* uL, const double* uR, const EState& L, const EState& R,
+                                     int axis, const Phys& P, double* F, unsigned& errbits) {
   constexpr int NC = DIM + 2;
-  const EState L = euler_state<DIM>(uL, axis, P);
-  const EState R = euler_state<DIM>(uR, axis, P);
-  const double sL = np_min(L.v - L.c, R.v - R.c);
-  const double sR = np_max(L.v + L.c, R.v + R.c);
-  if (sR - sL <= 0.0) errbits |= 1u;
-
+  const unsigned am = __activemask();
   bool equal = true;
 #pragma unroll
   for (int c = 0; c < NC; ++c) equal &= (uL[c] == uR[c]);
-
-  if (equal || sL >= 0.0) {
+  const double sL = np_min(L.v - L.c, R.v - R.c);
+  const double sR = np_max(L.v + L.c, R.v + R.c);
+  if (sR - sL <= 0.0) errbits |= 1u;
+  if (!__any_sync(am, !equal)) {  // whole warp: F(u, u) = f(u)
     euler_flux<DIM>(uL, L.p, L.v, axis, F);
     return;
   }
   const double den = L.rho * (sL - L.v) - R.rho * (sR - R.v);
 #if FVB_FAST
-  const double sM = (fma(L.rho * L.v, sL - L.v, R.p - L.p) - R.rho * R.v * (sR - R.v)) / den;
+  const double sM = fdiv(fma(L.rho * L.v, sL - L.v, R.p - L.p) - R.rho * R.v * (sR - R.v), den);
 #else
   const double sM = (R.p - L.p + L.rho * L.v * (sL - L.v) - R.rho * R.v * (sR - R.v)) / den;
 #endif
-  const double* u;
-  const EState* S;
-  double sK;
-  if (sM >= 0.0) {
-    u = uL; S = &L; sK = sL;
-  } else if (sR > 0.0) {
-    u = uR; S = &R; sK = sR;
-  } else {
-    euler_flux<DIM>(uR, R.p, R.v, axis, F);
-    return;
-  }
-  double f[NC];
-  euler_flux<DIM>(u, S->p, S->v, axis, f);
-  // star state (numerics.py:173-181)
+  const bool left = equal || (sL >= 0.0) || (sM >= 0.0);
+  const bool star = !equal && !(sL >= 0.0) && ((sM >= 0.0) || (sR > 0.0));
+  double u[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) u[c] = left ? uL[c] : uR[c];
+  const double rho = left ? L.rho : R.rho;
+  const double v = left ? L.v : R.v;
+  const double p = left ? L.p : R.p;
+  const double sK = left ? sL : sR;
+  euler_flux<DIM>(u, p, v, axis, F);
+  if (!__any_sync(am, star)) return;
+  // star state (numerics.py:173-181), evaluated for the selected side only
   double st[NC];
 #if FVB_FAST
-  const double sKv = sK - S->v;
-  const double rs = S->rho * sKv;
-  const double fac = rs / (sK - sM);
-  const double rinv = 1.0 / S->rho;
+  const double rinv = left ? L.rinv : R.rinv;
+  const double sKv = sK - v;
+  const double rs = rho * sKv;
+  const double fac = rs * frcp(sK - sM);
   st[0] = fac;
 #pragma unroll
   for (int j = 0; j < DIM; ++j) st[1 + j] = fac * (u[1 + j] * rinv);
   st[1 + axis] = fac * sM;
-  st[1 + DIM] = fac * fma(sM - S->v, sM + S->p / rs, u[1 + DIM] * rinv);
+  st[1 + DIM] = fac * fma(sM - v, fma(p, frcp(rs), sM), u[1 + DIM] * rinv);
 #pragma unroll
-  for (int c = 0; c < NC; ++c) F[c] = fma(sK, st[c] - u[c], f[c]);
+  for (int c = 0; c < NC; ++c) F[c] = star ? fma(sK, st[c] - u[c], F[c]) : F[c];
 #else
-  const double fac = S->rho * (sK - S->v) / (sK - sM);
+  const double fac = rho * (sK - v) / (sK - sM);
   st[0] = fac;
 #pragma unroll
   for (int j = 0; j < DIM; ++j) {
-    if (j != axis) st[1 + j] = fac * (u[1 + j] / S->rho);
+    if (j != axis) st[1 + j] = fac * (u[1 + j] / rho);
   }
   st[1 + axis] = fac * sM;
-  st[1 + DIM] = fac * (u[1 + DIM] / S->rho + (sM - S->v) * (sM + S->p / (S->rho * (sK - S->v))));
+  st[1 + DIM] = fac * (u[1 + DIM] / rho + (sM - v) * (sM + p / (rho * (sK - v))));
 #pragma unroll
-  for (int c = 0; c < NC; ++c) F[c] = f[c] + sK * (st[c] - u[c]);
+  for (int c = 0; c < NC; ++c) F[c] = star ? F[c] + sK * (st[c] - u[c]) : F[c];
 #endif
 }
 
-// Positivity fallback (solver.py:116-125): Euler + WENO only.  If either
-// reconstructed state is unphysical, both become the adjacent cell values.
-template <int EQ, int DIM, int RECON>
-__device__ __forceinline__ void fallback(double* uL, double* uR, const double* cL, const double* cR,
-                                         const Phys& P) {
-  if constexpr (EQ == EQ_EULER && RECON != RECON_NONE) {
-    constexpr int NC = DIM + 2;
-    if (!(euler_physical<DIM>(uL, P) & euler_physical<DIM>(uR, P))) {
+// Interface flux with the positivity fallback (solver.py:116-125; Euler +
+// WENO only): if either reconstructed state is unphysical, both become the
+// adjacent cell values cL, cR.  The physical check reuses the per-state
+// pressure the flux needs anyway (same expression -> exact mode bitwise).
+template <int EQ, int FLUX, int DIM, int RECON>
+__device__ __forceinline__ void interface_flux(const double* uL0, const double* uR0, const double* cL,
+                                               const double* cR, int axis, const Phys& P, double* F,
+                                               unsigned& errbits) {
+  constexpr int NC = NComp<EQ, DIM>::value;
+  if constexpr (EQ == EQ_EULER) {
+    double uL[NC], uR[NC];
 #pragma unroll
-      for (int c = 0; c < NC; ++c) { uL[c] = cL[c]; uR[c] = cR[c]; }
+    for (int c = 0; c < NC; ++c) { uL[c] = uL0[c]; uR[c] = uR0[c]; }
+    EState L = euler_state<DIM>(uL, axis, P);
+    EState R = euler_state<DIM>(uR, axis, P);
+    if constexpr (RECON != RECON_NONE) {
+      const bool ok = (uL[0] > kFloor) & (L.p > kFloor) & (uR[0] > kFloor) & (R.p > kFloor);
+      if (!ok) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) { uL[c] = cL[c]; uR[c] = cR[c]; }
+        L = euler_state<DIM>(uL, axis, P);
+        R = euler_state<DIM>(uR, axis, P);
+      }
     }
-  }
-}
-
-template <int EQ, int FLUX, int DIM>
-__device__ __forceinline__ void num_flux(const double* uL, const double* uR, int axis,
-                                         const Phys& P, double* F, unsigned& errbits) {
-  if constexpr (FLUX == FLUX_HLLC && EQ == EQ_EULER) {
-    hllc<DIM>(uL, uR, axis, P, F, errbits);
+    if constexpr (FLUX == FLUX_HLLC) hllc<DIM>(uL, uR, L, R, axis, P, F, errbits);
+    else rusanov<EQ, DIM>(uL, uR, L, R, axis, P, F);
   } else {
-    rusanov<EQ, DIM>(uL, uR, axis, P, F);
+    EState dummy{};
+    rusanov<EQ, DIM>(uL0, uR0, dummy, dummy, axis, P, F);
   }
 }
 
@@ -280,9 +316,12 @@ template <int EQ, int DIM>
 __device__ __forceinline__ void wave_speeds(const double* u, const Phys& P, double* s) {
   if constexpr (EQ == EQ_EULER) {
 #if FVB_FAST
-    const double r = 1.0 / u[0];
-    const double p = euler_pressure<DIM>(u, P);
-    const double c = sqrt(P.gamma * p * r);
+    const double r = frcp(u[0]);
+    double msq = u[1] * u[1];
+#pragma unroll
+    for (int k = 1; k < DIM; ++k) msq = fma(u[1 + k], u[1 + k], msq);
+    const double p = P.gm1 * fma(-0.5 * msq, r, u[1 + DIM]);
+    const double c = fsqrt(P.gamma * p * r);
 #pragma unroll
     for (int k = 0; k < DIM; ++k) s[k] = fabs(u[1 + k] * r) + c;
 #else

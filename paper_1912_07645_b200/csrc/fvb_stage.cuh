@@ -249,9 +249,8 @@ stage_kernel(const StageParams p) {
           double uL[NC], uR[NC], G[NC];
 #pragma unroll
           for (int c = 0; c < NC; ++c) { uL[c] = hiP[c]; uR[c] = loC[c]; }
-          fallback<EQ, DIM, RECON>(uL, uR, A, B, p.P);
           unsigned eb = 0;
-          num_flux<EQ, FLUX, DIM>(uL, uR, MA, p.P, G, eb);
+          interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, A, B, MA, p.P, G, eb);
           if (eb) errb |= 1u << MA;
           if (r - 1 >= ra) {
             double v[NC];
@@ -337,9 +336,8 @@ stage_kernel(const StageParams p) {
             uR[c] = cr[c];
           }
         }
-        fallback<EQ, DIM, RECON>(uL, uR, cl, cr, p.P);
         unsigned eb = 0;
-        num_flux<EQ, FLUX, DIM>(uL, uR, 0, p.P, G, eb);
+        interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 0, p.P, G, eb);
         if (eb && xf <= nx && (!PY || yf < ny)) errb |= 1u;
 #pragma unroll
         for (int c = 0; c < NC; ++c) sGx(c, ty, tx) = G[c];
@@ -359,9 +357,8 @@ stage_kernel(const StageParams p) {
               uR[c] = cr[c];
             }
           }
-          fallback<EQ, DIM, RECON>(uL, uR, cl, cr, p.P);
           unsigned eb = 0;
-          num_flux<EQ, FLUX, DIM>(uL, uR, 1, p.P, G, eb);
+          interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 1, p.P, G, eb);
           if (eb && yf <= ny && xf < nx) errb |= 2u;
 #pragma unroll
           for (int c = 0; c < NC; ++c) sGy(c, ty, tx) = G[c];
@@ -432,6 +429,234 @@ constexpr int stage_smem_bytes() {
               ((WENO && PY) ? 2 : 0) * NC * NTY * NT + (PY ? NC * NTY * NT : 0));
 }
 
+// ---------------------------------------------------------------------------
+// Warp-strip kernel (1D and 2D): the production path for the 2D configs.
+//
+// Each WARP owns a strip of 30 cells in x (lanes 1..30; lanes 0 and 31 are
+// the halo face cells) and marches along y over one chunk of rows.  x
+// neighbours are exchanged with warp shuffles, so there is no shared memory
+// and no block barrier at all; y uses the per-thread register window.  The
+// row loop is unrolled by 4 with the window arrays rotated by name, so no
+// register moves are spent on the march.
+// ---------------------------------------------------------------------------
+constexpr int kStripCells = 30;
+#ifndef FVB_STRIP_MINB
+#define FVB_STRIP_MINB 4
+#endif
+
+template <int NC>
+__device__ __forceinline__ void shfl_up_nc(const double* v, double* out) {
+#pragma unroll
+  for (int c = 0; c < NC; ++c) out[c] = __shfl_up_sync(0xffffffffu, v[c], 1);
+}
+template <int NC>
+__device__ __forceinline__ void shfl_down_nc(const double* v, double* out) {
+#pragma unroll
+  for (int c = 0; c < NC; ++c) out[c] = __shfl_down_sync(0xffffffffu, v[c], 1);
+}
+
+template <int DIM, int EQ, int FLUX, int RECON>
+struct StripCtx {
+  static constexpr int NC = NComp<EQ, DIM>::value;
+  const StageParams& p;
+  FvbState* st;
+  const double* __restrict__ us;
+  const double* un;
+  double* out;
+  double dt;
+  int lane;
+  int64_t x0, xf;
+  bool cell;
+  int64_t ra, rb;
+  unsigned errb;
+  double smax[DIM];
+  int64_t xo;   // mapped x offset of this lane's column
+  int64_t hxo;  // mapped x offset of the halo column (lanes 0 and 31)
+
+  __device__ __forceinline__ int64_t roff(int64_t r) const {
+    if constexpr (DIM == 1) return 0;
+    else return map_index(r, p.n[1], p.bc[1], p.g) * p.sy;
+  }
+  __device__ __forceinline__ int64_t off(int64_t x, int64_t r) const {
+    return map_index(x, p.n[0], p.bc[0], p.g) + roff(r);
+  }
+  __device__ __forceinline__ void load_row(int64_t r, double* v) const { load_nc<NC>(us, xo + roff(r), p.sc, v); }
+  // halo value: lane 0 -> x0-2, lane 31 -> x0+31 (WENO only)
+  __device__ __forceinline__ void load_halo(int64_t r, double* v) const {
+    if constexpr (RECON != RECON_NONE) {
+      if (lane == 0 || lane == 31) load_nc<NC>(us, hxo + roff(r), p.sc, v);
+    }
+  }
+
+  // x direction of one row: returns the in-plane residual of this lane's cell
+  __device__ __forceinline__ void xrow(const double* uc, const double* halo, double* res) {
+    double um[NC], up[NC], hi[NC], lo[NC], hiL[NC], G[NC], Gn[NC];
+    shfl_up_nc<NC>(uc, um);
+    shfl_down_nc<NC>(uc, up);
+    if constexpr (RECON != RECON_NONE) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        if (lane == 0) um[c] = halo[c];
+        if (lane == 31) up[c] = halo[c];
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) weno_faces<RECON>(um[c], uc[c], up[c], p.P.eps, hi[c], lo[c]);
+      shfl_up_nc<NC>(hi, hiL);
+    } else {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) { hiL[c] = um[c]; lo[c] = uc[c]; }
+    }
+    // interface (lane-1 | lane): uL = high face of lane-1, uR = low face of lane
+    double uL[NC], uR[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) { uL[c] = hiL[c]; uR[c] = lo[c]; }
+    unsigned eb = 0;
+    interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, um, uc, 0, p.P, G, eb);
+    if (eb && lane >= 1 && xf <= p.n[0]) errb |= 1u;
+    shfl_down_nc<NC>(G, Gn);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+#if FVB_FAST
+      res[c] = (G[c] - Gn[c]) * p.id[0];
+#else
+      res[c] = 0.0 - ddiv(Gn[c] - G[c], p, 0);
+#endif
+    }
+  }
+
+  __device__ __forceinline__ void finish(int64_t r, const double* usc, const double* unc, const double* Lc) {
+    double v[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) v[c] = rk_combine(p.kind, unc[c], usc[c], dt, Lc[c]);
+    const int64_t o = xo + roff(r);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
+    if (p.final_stage) post_cell<EQ, DIM, NC>(p, st, v, xf, DIM == 2 ? r : 0, 0, smax);
+  }
+
+  __device__ __forceinline__ void stage_check(int64_t r, const double* uc) {
+    if constexpr (EQ == EQ_EULER) {
+      if (cell && !euler_physical<DIM>(uc, p.P)) {
+        const long long key = ((long long)p.stage_idx << 42) | flat_cell<DIM>(p, xf, DIM == 2 ? r : 0, 0);
+        atomicMin(&st->stage_err, key);
+      }
+    }
+  }
+
+  // One march row r.  On entry A,B,C = u[r-1], u[r], u[r+1]; on exit A
+  // holds u[r+2] (loaded once A is dead), so the caller rotates (B, C, A).
+  // H: high y-face of row r-1 -> r;  G: y flux (r-2|r-1) -> (r-1|r);
+  // R: x residual of row r-1 -> r.
+  __device__ __forceinline__ void row(int64_t r, double* A, const double* B, const double* C,
+                                      double* H, double* G, double* R) {
+    const bool in_row = r >= ra && r < rb;
+    double halo[NC], unc[NC];
+    if (in_row) load_halo(r, halo);
+    const bool fin = cell && r - 1 >= ra;
+    if (fin && p.kind >= 2) {
+      const int64_t o = xo + roff(r - 1);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) unc[c] = un[o + c * p.sc];
+    }
+    if (cell) {
+      double hi[NC], lo[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) weno_faces<RECON>(A[c], B[c], C[c], p.P.eps, hi[c], lo[c]);
+      if (r >= ra) {
+        double uL[NC], uR[NC], GC[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) { uL[c] = H[c]; uR[c] = lo[c]; }
+        unsigned eb = 0;
+        interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, A, B, 1, p.P, GC, eb);
+        if (eb) errb |= 2u;
+        if (fin) {
+          double Lc[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+#if FVB_FAST
+            Lc[c] = fma(G[c] - GC[c], p.id[1], R[c]);
+#else
+            Lc[c] = R[c] - ddiv(GC[c] - G[c], p, 1);
+#endif
+          }
+          finish(r - 1, A, unc, Lc);
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) G[c] = GC[c];
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) H[c] = hi[c];
+    }
+    if (r + 2 <= rb + 1) load_row(r + 2, A);  // A is dead: prefetch the row after next
+    if (in_row) {
+      stage_check(r, B);
+      xrow(B, halo, R);
+    }
+  }
+};
+
+template <int DIM, int EQ, int FLUX, int RECON, int WPB>
+__global__ void __launch_bounds__(32 * WPB, FVB_STRIP_MINB)
+strip_kernel(const StageParams p) {
+  using S = StripCtx<DIM, EQ, FLUX, RECON>;
+  constexpr int NC = S::NC;
+  const int lane = threadIdx.x & 31;
+  const int64_t strip = (int64_t)blockIdx.x * WPB + (threadIdx.x >> 5);
+  const int inst = blockIdx.z;
+  FvbState* st = p.st + inst;
+  if (*(volatile int*)&st->done) return;  // uniform over the grid
+  const int64_t x0 = strip * kStripCells;
+  S s{p, st, p.us + p.origin + inst * p.si, p.un + p.origin + inst * p.si, p.out + p.origin + inst * p.si,
+      p.kind == 0 ? 0.0 : *(volatile double*)&st->dt, lane, x0, x0 - 1 + lane, false, 0, 1, 0u, {},
+      map_index(x0 - 1 + lane, p.n[0], p.bc[0], p.g),
+      map_index(lane == 0 ? x0 - 2 : x0 + 31, p.n[0], p.bc[0], p.g)};
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) s.smax[k] = 0.0;
+  const bool active = x0 < p.n[0];  // warp-uniform
+  if (active) {
+    s.cell = lane >= 1 && lane <= kStripCells && s.xf < p.n[0];
+    if constexpr (DIM == 1) {
+      double B[NC], halo[NC], res[NC], unc[NC];
+      s.load_row(0, B);
+      s.load_halo(0, halo);
+      s.stage_check(0, B);
+      s.xrow(B, halo, res);
+      if (s.cell) {
+        if (p.kind >= 2) {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) unc[c] = s.un[s.xo + c * p.sc];
+        }
+        s.finish(0, B, unc, res);
+      }
+    } else {
+      s.ra = (int64_t)blockIdx.y * p.H;
+      s.rb = min(s.ra + (int64_t)p.H, p.n[1]);
+      double W0[NC], W1[NC], W2[NC], H[NC], G[NC], R[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) H[c] = G[c] = R[c] = 0.0;
+      const int64_t ra = s.ra, rb = s.rb;
+      s.load_row(ra - 2, W0);
+      s.load_row(ra - 1, W1);
+      s.load_row(ra, W2);
+      // rows r = ra-1 .. rb, window rotated by name (period 3)
+      for (int64_t r = ra - 1; r <= rb; r += 3) {
+        s.row(r, W0, W1, W2, H, G, R);
+        if (r + 1 > rb) break;
+        s.row(r + 1, W1, W2, W0, H, G, R);
+        if (r + 2 > rb) break;
+        s.row(r + 2, W2, W0, W1, H, G, R);
+      }
+    }
+    if (s.errb) {
+#pragma unroll
+      for (int a = 0; a < DIM; ++a)
+        if (s.errb & (1u << a))
+          atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | ((long long)(1 + a) << 40));
+    }
+  }
+  if (p.final_stage) block_epilogue<DIM>(p, st, inst, s.smax, true);
+}
+
 // Standalone wave-speed pass: solver.py:128-136 (+ the initial is_physical
 // check of solver.py:211-212).  finalize = 1 also computes the first dt.
 template <int DIM, int EQ>
@@ -489,7 +714,7 @@ __global__ void __launch_bounds__(256) speed_kernel(const StageParams p, int fin
 // host-side launchers (defined in fvb_kernels.cu, once per namespace)
 int launch_stage(int dim, int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s);
 int launch_speed(int dim, int eq, const StageParams& p, int finalize, dim3 grid, cudaStream_t s);
-void stage_block(int dim, int& nt, int& nty);
+void stage_block(int dim, int variant, int& nt, int& nty);
 
 }  // namespace FVB_NS
 }  // namespace fvb

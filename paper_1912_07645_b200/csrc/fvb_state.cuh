@@ -152,6 +152,7 @@ struct StageParams {
   int chunks;         // chunks along the march axis
   int H;              // rows per chunk
   unsigned nblocks;   // blocks per instance (finalize counter)
+  int variant;        // 1D/2D kernel: 0 = warp strip, 1 = shared-memory tile
   LoopCtl ctl;
 };
 

@@ -346,8 +346,15 @@ def run_simulation(init, cfg, observers: Sequence[Callable] = (), max_steps: int
         infos, done = run.poll()
         if infos[0].err or done[0]:
             break
+        n = step_batch
+        if max_steps is not None:
+            n = min(n, max(1, int(max_steps) - int(infos[0].steps)))
+        if infos[0].dt > 0 and not observers:
+            # about the steps left to t_end (+ slack); extra launches exit early
+            left = (cfg.t_end - infos[0].t) / infos[0].dt
+            n = int(min(n, max(1, math.ceil(left) + 2)))
         tic = time.perf_counter()
-        run.steps(step_batch)
+        run.steps(n)
         infos, done = run.poll()
         secs = (time.perf_counter() - tic) / max(1, infos[0].steps - run._seen[0])
         run.read_log(infos, secs)

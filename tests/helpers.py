@@ -13,6 +13,23 @@ def oracle_scheme(d: dict) -> O.Scheme:
     )
 
 
+def rel_l1_field(a, b):
+    """Per-component relative L1 errors, max over components.  A component
+    whose L1 norm is below 1e-6 of the largest component's is round-off
+    (e.g. the transverse momentum of a 2D-invariant 3D state); its error is
+    measured relative to the largest component's norm instead."""
+    a = np.asarray(a, dtype=float)
+    b = np.asarray(b, dtype=float)
+    norms = [np.abs(b[c]).sum() for c in range(b.shape[0])]
+    big = max(norms) if norms else 0.0
+    worst = 0.0
+    for c in range(b.shape[0]):
+        den = max(norms[c], 1e-6 * big)
+        err = np.abs(a[c] - b[c]).sum()
+        worst = max(worst, err / den if den else err)
+    return float(worst)
+
+
 def rel_l1(a, b):
     a = np.asarray(a, dtype=float)
     b = np.asarray(b, dtype=float)

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from oracle import fv_oracle as O
-from tests.helpers import oracle_scheme, product_objects, rel_l1
+from tests.helpers import oracle_scheme, product_objects, rel_l1, rel_l1_field
 
 pytestmark = pytest.mark.gpu
 
@@ -61,11 +61,10 @@ def test_run_simulation_fast_tolerance(P, golden, golden_arrays, name):
     ref = golden_arrays[name + "__final"]
     sc = oracle_scheme(case["scheme"])
     ref_in = O.interior(ref, sc)
-    assert abs(len(recs) - case["steps"]) <= 1
-    n = min(len(recs), case["steps"])
-    for c in range(ref_in.shape[0]):
-        if len(recs) == case["steps"]:
-            assert rel_l1(final.interior[c], ref_in[c]) <= TOL_FAST, (name, c)
+    assert len(recs) == case["steps"], name
+    err = rel_l1_field(final.interior, ref_in)
+    print(f"{name}: fast-mode relative L1 = {err:.3e}")
+    assert err <= TOL_FAST, (name, err)
 
 
 def test_residual_and_maxima_bitwise(P, golden, golden_arrays):
@@ -163,3 +162,28 @@ def test_device_field_roundtrip(P, golden, golden_arrays):
     out, recs = P.run_simulation(dev, cfg, max_steps=50)
     assert isinstance(out, P.DeviceField)
     assert O.sha16(out.interior.cpu().numpy()) == case["final_sha"]
+
+
+@pytest.mark.parametrize("name", ["kh2d32_weno3_20", "kh3d16_weno2_5", "kh2d64_weno2_50"])
+def test_fast_mode_divergence_growth(P, golden, golden_arrays, name):
+    """Fast arithmetic differs from the reference by rounding (~1 ulp per
+    operation); Kelvin-Helmholtz amplifies such differences.  Report the
+    relative L1 distance to the bitwise oracle after 1..N steps and check the
+    first step is at rounding level."""
+    case = next(r for r in golden["runs"] if r["name"] == name)
+    grid, cfg = product_objects(case["scheme"])
+    init = _init_field(P, case, golden_arrays, grid)
+    sc = oracle_scheme(case["scheme"])
+    cur = init.data.copy()
+    rows = []
+    n = case["max_steps"]
+    marks = sorted({1, 2, 3, 5, 10, 20, 50, n} & set(range(1, n + 1)))
+    for m in marks:
+        final, _ = P.run_simulation(init, cfg, max_steps=m, arith="fast")
+        ref, _ = O.simulate(init.data, sc, m)
+        ref_in = O.interior(ref, sc)
+        per = [rel_l1(final.interior[c], ref_in[c]) for c in range(ref_in.shape[0])]
+        rows.append((m, rel_l1_field(final.interior, ref_in), per))
+    for m, e, per in rows:
+        print(f"{name} steps={m:3d} rel_l1_field={e:.3e} per-component={['%.2e' % x for x in per]}")
+    assert rows[0][1] <= 1e-13
