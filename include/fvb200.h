@@ -51,7 +51,10 @@ enum { FVB_EQ_EULER = 0, FVB_EQ_BURGERS = 1, FVB_EQ_ADVECTION = 2 };
 enum { FVB_FLUX_RUSANOV = 0, FVB_FLUX_HLLC = 1 };
 enum { FVB_RECON_NONE = 0, FVB_RECON_WENO2 = 1, FVB_RECON_WENO3 = 2 };
 enum { FVB_BC_PERIODIC = 0, FVB_BC_OUTFLOW = 1, FVB_BC_HALO = 2 };
-enum { FVB_MODE_T_END = 0, FVB_MODE_FIXED = 1 };
+/* T_END: run_simulation (solver.py:199-246); FIXED: run_parallel n_steps;
+ * PAR_T_END: run_parallel without n_steps (parallel.py:490-520: t_end loop,
+ * finiteness-only post-step check) */
+enum { FVB_MODE_T_END = 0, FVB_MODE_FIXED = 1, FVB_MODE_PAR_T_END = 2 };
 enum { FVB_ARITH_EXACT = 0, FVB_ARITH_FAST = 1 };
 
 /* SchemeConfig + GridSpec + EquationModel (solver.py:36-44, grid.py:39-50,
@@ -150,6 +153,14 @@ int fvb_run_set_log(fvb_ctx* ctx, int64_t per_instance, int ninst);
 /* copy the step-log ring of the active run: entry (inst, (step-1) % per_instance)
  * holds (t, dt) of that step; h_log has 2*ninst*per_instance doubles */
 int fvb_run_read_log(fvb_ctx* ctx, double* h_log, int64_t per_instance);
+/* parallel.py:430-521 on one device: the ninst instances of the next
+ * fvb_run_begin are the subdomains of ONE run on a Cartesian rank grid
+ * (ranks[3], x fastest, parallel.py:45-89).  Axes with ranks > 1 must be
+ * FVB_BC_HALO in the scheme; a face-only halo kernel fills their ghosts
+ * before every stage (periodic[k]: wrap at the world edge, else outflow).
+ * All instances share one step state (global dt = max over subdomains,
+ * parallel.py:498-501).  ranks = NULL clears. */
+int fvb_run_set_topology(fvb_ctx* ctx, const int32_t* ranks, const int32_t* periodic);
 /* kernel launches issued by the last fvb_run / fvb_run_steps calls */
 int64_t fvb_launch_count(const fvb_ctx* ctx);
 

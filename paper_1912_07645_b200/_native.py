@@ -23,7 +23,7 @@ EQ = {"euler": 0, "burgers": 1, "advection": 2}
 FLUX = {"rusanov": 0, "hllc": 1}
 RECON = {"none": 0, "weno2": 1, "weno3": 2}
 BC_PERIODIC, BC_OUTFLOW, BC_HALO = 0, 1, 2
-MODE_T_END, MODE_FIXED = 0, 1
+MODE_T_END, MODE_FIXED, MODE_PAR_T_END = 0, 1, 2
 ARITH = {"exact": 0, "fast": 1}
 
 
@@ -77,6 +77,7 @@ _SIGS = {
     "fvb_run_end": ([C.c_void_p, C.POINTER(RunInfo), C.POINTER(C.c_double), C.c_int64], C.c_int),
     "fvb_run_poll": ([C.c_void_p, C.POINTER(RunInfo), C.POINTER(C.c_int32)], C.c_int),
     "fvb_run_set_log": ([C.c_void_p, C.c_int64, C.c_int], C.c_int),
+    "fvb_run_set_topology": ([C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)], C.c_int),
     "fvb_run_read_log": ([C.c_void_p, C.POINTER(C.c_double), C.c_int64], C.c_int),
     "fvb_launch_count": ([C.c_void_p], C.c_int64),
     "fvb_moments_push": ([C.c_void_p, C.POINTER(Scheme), C.POINTER(Layout), C.c_void_p, C.c_int,

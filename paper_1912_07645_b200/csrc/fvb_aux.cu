@@ -218,6 +218,67 @@ __global__ void structure_pass2(const double* __restrict__ partials, int nblocks
   }
 }
 
+// Face-only halo exchange between subdomain instances of one buffer
+// (parallel.py:201-254 with the corner passes dropped: the residual crops
+// transverse axes to the interior, solver.py:99-104, so corners are never
+// read).  Instance i is rank i of a Cartesian topology, x fastest
+// (parallel.py:66-77).  Ghosts on split axes come from the neighbour's
+// interior (periodic wrap at the world edge) or, at a non-periodic world
+// edge, from the nearest own interior cell (parallel.py:189-198).
+struct Topo {
+  int r[3];       // ranks per axis
+  int periodic[3];
+};
+
+__global__ void halo_instances_kernel(Pad p, fvb_layout L, double* u, int ncomp, int ninst, Topo T) {
+  const int64_t nx = p.n[0], ny = p.n[1], nz = p.n[2];
+  const int g = p.g;
+  int64_t per_axis[3];
+  per_axis[0] = (T.r[0] > 1) ? 2LL * g * ny * nz : 0;
+  per_axis[1] = (T.r[1] > 1) ? 2LL * g * nx * nz : 0;
+  per_axis[2] = (T.r[2] > 1) ? 2LL * g * nx * ny : 0;
+  const int64_t per_comp = per_axis[0] + per_axis[1] + per_axis[2];
+  const int64_t total = per_comp * ncomp * ninst;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t q = i % per_comp;
+    const int64_t cc = i / per_comp;
+    const int c = (int)(cc % ncomp);
+    const int inst = (int)(cc / ncomp);
+    int axis = 0;
+    while (q >= per_axis[axis]) { q -= per_axis[axis]; ++axis; }
+    const int a1 = axis == 0 ? 1 : 0, a2 = axis == 2 ? 1 : 2;
+    const int64_t t0 = q % p.n[a1];
+    q /= p.n[a1];
+    const int64_t t1 = q % p.n[a2];
+    q /= p.n[a2];
+    const int j = (int)(q % g);
+    const int side = (int)(q / g);
+    int nb[3] = {inst % T.r[0], (inst / T.r[0]) % T.r[1], inst / (T.r[0] * T.r[1])};
+    const int64_t n = p.n[axis];
+    int64_t src_a;
+    int src_inst;
+    nb[axis] += side == 0 ? -1 : 1;
+    if ((nb[axis] < 0 || nb[axis] >= T.r[axis]) && !T.periodic[axis]) {
+      src_inst = inst;                 // outflow world edge: nearest own interior cell
+      src_a = side == 0 ? 0 : n - 1;
+    } else {
+      nb[axis] = (nb[axis] + T.r[axis]) % T.r[axis];
+      src_inst = nb[0] + T.r[0] * (nb[1] + T.r[1] * nb[2]);
+      src_a = side == 0 ? n - g + j : j;   // neighbour's interior slab
+    }
+    const int64_t dst_a = side == 0 ? (int64_t)j - g : n + j;
+    int64_t d3[3], s3[3];
+    d3[axis] = dst_a;
+    s3[axis] = src_a;
+    d3[a1] = s3[a1] = t0;
+    d3[a2] = s3[a2] = t1;
+    const int64_t od = d3[0] + (p.dim >= 2 ? d3[1] * L.sy : 0) + (p.dim >= 3 ? d3[2] * L.sz : 0);
+    const int64_t os = s3[0] + (p.dim >= 2 ? s3[1] * L.sy : 0) + (p.dim >= 3 ? s3[2] * L.sz : 0);
+    double* base = u + L.origin + c * L.sc;
+    base[inst * L.si + od] = base[src_inst * L.si + os];
+  }
+}
+
 int grid_for(int64_t n) {
   int64_t b = (n + 255) / 256;
   if (b > 148 * 16) b = 148 * 16;
@@ -249,6 +310,23 @@ int launch_halo(const fvb_scheme& s, const fvb_layout& L, double* u, int axis, i
   const Pad p = make_pad(s);
   halo_kernel<<<grid_for(halo_count(s, axis)), 256, 0, st>>>(p, L, u, s.ncomp, axis, side, buf, unpack);
   return 0;
+}
+
+int launch_halo_instances(const fvb_scheme& s, const fvb_layout& L, double* u, int ninst, const int* ranks,
+                          const int* periodic, cudaStream_t st) {
+  const Pad p = make_pad(s);
+  Topo T;
+  int64_t per = 0;
+  for (int k = 0; k < 3; ++k) {
+    T.r[k] = k < s.dim ? ranks[k] : 1;
+    T.periodic[k] = periodic[k];
+  }
+  if (T.r[0] > 1) per += 2LL * p.g * p.n[1] * p.n[2];
+  if (T.r[1] > 1) per += 2LL * p.g * p.n[0] * p.n[2];
+  if (T.r[2] > 1) per += 2LL * p.g * p.n[0] * p.n[1];
+  if (per == 0) return 0;
+  halo_instances_kernel<<<grid_for(per * s.ncomp * ninst), 256, 0, st>>>(p, L, u, s.ncomp, ninst, T);
+  return 1;
 }
 
 int launch_moments_push(const fvb_scheme& s, const fvb_layout& L, const double* u, int inst, double* mean,

@@ -39,6 +39,8 @@ int launch_moments_merge(double* ma, double* m2a, int64_t ca, const double* mb, 
 int launch_structure(const fvb_scheme& s, const fvb_layout& L, const double* u, int inst, int comp, double p,
                      int H, double* d_sums, double* d_partials, int nblocks, cudaStream_t st);
 int structure_blocks(const fvb_scheme& s);
+int launch_halo_instances(const fvb_scheme& s, const fvb_layout& L, double* u, int ninst, const int* ranks,
+                          const int* periodic, cudaStream_t st);
 }  // namespace fvb
 
 using fvb::FvbState;
@@ -57,6 +59,9 @@ struct RunPlan {
   int nstages;
   dim3 grid;
   int active;
+  int topo;          // instances are the subdomains of one decomposed run
+  int ranks[3];
+  int periodic[3];
 };
 
 struct fvb_ctx {
@@ -74,6 +79,9 @@ struct fvb_ctx {
   double* d_partials;
   int64_t partials_cap;
   RunPlan plan;
+  int topo_pending;
+  int topo_ranks[3];
+  int topo_periodic[3];
   cudaGraphExec_t graph;
   int graph_steps;
   int graph_parity_ok;
@@ -470,6 +478,14 @@ int fvb_ssp_rk_step(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, do
 // Device-resident run loop
 // ---------------------------------------------------------------------------
 
+static int do_halo(fvb_ctx* ctx, const double* us) {
+  RunPlan& P = ctx->plan;
+  if (!P.topo) return FVB_OK;
+  if (fvb::launch_halo_instances(P.s, P.L, const_cast<double*>(us), P.ninst, P.ranks, P.periodic, ctx->stream))
+    ctx->launches++;
+  return check_launch(ctx, "halo_instances");
+}
+
 static int enqueue_step(fvb_ctx* ctx) {
   RunPlan& P = ctx->plan;
   if (P.s.rk_order == 1) {
@@ -478,11 +494,15 @@ static int enqueue_step(fvb_ctx* ctx) {
     p.us = P.bufs[par];
     p.un = P.bufs[par];
     p.out = P.bufs[1 - par];
-    int r = do_stage(ctx, P.s, p, P.grid);
+    int r = do_halo(ctx, p.us);
+    if (r) return r;
+    r = do_stage(ctx, P.s, p, P.grid);
     if (r) return r;
   } else {
     for (int i = 0; i < P.nstages; ++i) {
-      int r = do_stage(ctx, P.s, P.stage[i], P.grid);
+      int r = do_halo(ctx, P.stage[i].us);
+      if (r) return r;
+      r = do_stage(ctx, P.s, P.stage[i], P.grid);
       if (r) return r;
     }
   }
@@ -508,13 +528,25 @@ int fvb_run_begin(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, doub
   P.ninst = ninst;
   P.mode = mode;
   P.max_steps = max_steps;
+  P.topo = ctx->topo_pending;
+  ctx->topo_pending = 0;
+  for (int k = 0; k < 3; ++k) {
+    P.ranks[k] = ctx->topo_ranks[k];
+    P.periodic[k] = ctx->topo_periodic[k];
+  }
+  if (P.topo) {
+    int64_t nr = (int64_t)P.ranks[0] * P.ranks[1] * P.ranks[2];
+    if (nr != ninst) return set_err(ctx, FVB_E_CONFIG, "topology has %lld ranks but %d instances", (long long)nr, ninst);
+  }
   StageParams base = base_params(*s, *lay);
   base.st = ctx->d_state;
+  base.shared_state = P.topo;
   base.ctl.mode = mode;
   base.ctl.max_steps = mode == FVB_MODE_FIXED ? max_steps : max_steps;
   base.ctl.log = ctx->log_stride > 0 ? ctx->d_log : nullptr;
   base.ctl.log_cap = ctx->log_stride;
   P.grid = stage_grid(*s, base, ninst);
+  if (P.topo) base.nblocks *= (unsigned)ninst;  // one shared state counts every subdomain's blocks
   P.nstages = build_step(*s, *lay, P.bufs, base, P.stage);
   P.active = 1;
   // initial wave-speed pass + first dt (solver.py:211-224)
@@ -602,6 +634,20 @@ int fvb_run_read_log(fvb_ctx* ctx, double* h_log, int64_t per_instance) {
   CUDA_TRY(ctx, cudaMemcpyAsync(h_log, ctx->d_log, sizeof(double2) * per_instance * P.ninst, cudaMemcpyDeviceToHost,
                                 ctx->stream));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return FVB_OK;
+}
+
+int fvb_run_set_topology(fvb_ctx* ctx, const int32_t* ranks, const int32_t* periodic) {
+  if (!ranks) {
+    ctx->topo_pending = 0;
+    return FVB_OK;
+  }
+  for (int k = 0; k < 3; ++k) {
+    if (ranks[k] < 1) return set_err(ctx, FVB_E_CONFIG, "ranks per axis must be >= 1");
+    ctx->topo_ranks[k] = ranks[k];
+    ctx->topo_periodic[k] = periodic ? periodic[k] : 1;
+  }
+  ctx->topo_pending = 1;
   return FVB_OK;
 }
 

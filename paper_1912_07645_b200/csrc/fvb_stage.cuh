@@ -134,7 +134,7 @@ __device__ __forceinline__ void block_epilogue(const StageParams& p, FvbState* s
     const unsigned prev = atomicAdd(&st->blocks_done, 1u);
     if (prev == p.nblocks - 1) {
       __threadfence();
-      finalize_step(st, p.ctl, inst, post, true);
+      finalize_step(st, p.ctl, p.shared_state ? 0 : inst, post, true);
     }
   }
 }
@@ -186,7 +186,7 @@ stage_kernel(const StageParams p) {
     inst = blockIdx.z;
     chunk = 0;
   }
-  FvbState* st = p.st + inst;
+  FvbState* st = p.st + (p.shared_state ? 0 : inst);
   if (*(volatile int*)&st->done) return;  // uniform over the block
   const double dt = p.kind == 0 ? 0.0 : *(volatile double*)&st->dt;
 
@@ -603,7 +603,7 @@ strip_kernel(const StageParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t strip = (int64_t)blockIdx.x * WPB + (threadIdx.x >> 5);
   const int inst = blockIdx.z;
-  FvbState* st = p.st + inst;
+  FvbState* st = p.st + (p.shared_state ? 0 : inst);
   if (*(volatile int*)&st->done) return;  // uniform over the grid
   const int64_t x0 = strip * kStripCells;
   S s{p, st, p.us + p.origin + inst * p.si, p.un + p.origin + inst * p.si, p.out + p.origin + inst * p.si,
@@ -663,7 +663,7 @@ template <int DIM, int EQ>
 __global__ void __launch_bounds__(256) speed_kernel(const StageParams p, int finalize) {
   constexpr int NC = NComp<EQ, DIM>::value;
   const int inst = blockIdx.y;
-  FvbState* st = p.st + inst;
+  FvbState* st = p.st + (p.shared_state ? 0 : inst);
   const double* u = p.us + p.origin + inst * p.si;
   double smax[DIM];
 #pragma unroll
@@ -704,9 +704,9 @@ __global__ void __launch_bounds__(256) speed_kernel(const StageParams p, int fin
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned prev = atomicAdd(&st->blocks_done, 1u);
-    if (prev == gridDim.x - 1) {
+    if (prev == gridDim.x * (p.shared_state ? gridDim.y : 1u) - 1) {
       __threadfence();
-      finalize_step(st, p.ctl, inst, false, true);
+      finalize_step(st, p.ctl, p.shared_state ? 0 : inst, false, true);
     }
   }
 }

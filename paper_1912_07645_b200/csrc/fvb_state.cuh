@@ -89,9 +89,14 @@ __device__ inline void finalize_step(FvbState* st, const LoopCtl& L, int inst, b
     vs->errcell = vs->bad_unphys;
     stop = true;
   }
-  if (!stop && post && L.mode == FVB_MODE_FIXED && vs->bad_unphys != kNone) {
-    // next iteration's wave_speed_maxima(check=True) raises (equations.py:118-119)
-    if (vs->step < L.max_steps) {
+  const bool t_control = L.mode != FVB_MODE_FIXED;
+  if (!stop && post && L.mode != FVB_MODE_T_END && vs->bad_unphys != kNone) {
+    // run_parallel checks only finiteness after a step (parallel.py:518-519);
+    // the next iteration's wave_speed_maxima(check=True) raises
+    // (equations.py:118-119) -- if there is a next iteration
+    const bool more = t_control ? (vs->t < L.t_end && !(L.t_end - vs->t <= 1e-14 * L.t_end))
+                                : (vs->step < L.max_steps);
+    if (more) {
       vs->err = FVB_E_UNPHYSICAL;
       vs->errsub = FVB_SUB_SPEED_UNPHYSICAL;
       vs->errcell = vs->bad_unphys;
@@ -101,8 +106,8 @@ __device__ inline void finalize_step(FvbState* st, const LoopCtl& L, int inst, b
   double rem = 0.0;
   if (!stop) {
     const double t = vs->t;
-    if (L.mode == FVB_MODE_T_END) {
-      if (!(t < L.t_end)) stop = true;             // solver.py:219
+    if (t_control) {
+      if (!(t < L.t_end)) stop = true;             // solver.py:219 / parallel.py:495
       rem = L.t_end - t;                           // solver.py:220
       if (!stop && rem <= 1e-14 * L.t_end) stop = true;
       if (!stop && L.max_steps >= 0 && vs->step >= L.max_steps) stop = true;
@@ -119,7 +124,7 @@ __device__ inline void finalize_step(FvbState* st, const LoopCtl& L, int inst, b
       stop = true;
     } else {
       double dt = L.cfl / denom;
-      if (L.mode == FVB_MODE_T_END) dt = (rem < dt) ? rem : dt;  // min(dt, remaining)
+      if (t_control) dt = (rem < dt) ? rem : dt;  // min(dt, remaining)
       vs->dt = dt;
     }
   }
@@ -151,7 +156,8 @@ struct StageParams {
   int stage_idx;      // stage number within the step (error ordering)
   int chunks;         // chunks along the march axis
   int H;              // rows per chunk
-  unsigned nblocks;   // blocks per instance (finalize counter)
+  unsigned nblocks;   // blocks per state (finalize counter)
+  int shared_state;   // 1: all instances are subdomains of one run (one FvbState)
   int variant;        // 1D/2D kernel: 0 = warp strip, 1 = shared-memory tile
   LoopCtl ctl;
 };

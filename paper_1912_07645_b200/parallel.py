@@ -1,0 +1,351 @@
+"""Cartesian domain decomposition on the B200 path (parallel.py:45-547 of the
+reference).
+
+Two executions of ``run_parallel`` share one contract -- bitwise identical to
+the serial solver for every rank layout (tests/test_parallel.py:192-212 of
+the reference):
+
+* one device (default): the subdomains are instances of ONE batched device
+  run; before every stage a face-only halo kernel copies each subdomain's
+  boundary slabs into its neighbours' ghost cells, all subdomains share one
+  step state, so dt is the global max-reduction (parallel.py:498-501) and
+  the whole loop stays on the GPU (CUDA-graph batches, no host sync).
+* one process per GPU (``torch.distributed`` initialised, world size ==
+  number of ranks): ``run_parallel_nccl`` -- halo slabs packed by
+  fvb_halo_pack, exchanged with NCCL send/recv, unpacked by fvb_halo_unpack;
+  dt from an all-reduce(MAX) of the per-axis maxima.
+
+``exchange_halos`` keeps the reference's message-level API (sequential
+axes, full padded extents, tags) with device pack/unpack.
+"""
+
+from __future__ import annotations
+
+import math
+import queue
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from . import errors as E
+from .grid import BoundaryKind, Field, GridSpec, make_field
+from .solver import (DeviceField, DeviceRun, TYPES, _raise_run_error, _v, check_scheme, make_layout, make_scheme)
+
+_RECV_TIMEOUT = 60.0
+
+
+@dataclass(frozen=True)
+class RankTopology:
+    """Cartesian layout of ranks; rank 0 at the origin, x fastest."""
+
+    ranks_per_axis: tuple
+
+    def __post_init__(self):
+        object.__setattr__(self, "ranks_per_axis", tuple(int(r) for r in self.ranks_per_axis))
+        if any(r < 1 for r in self.ranks_per_axis):
+            raise E.ConfigError(f"ranks per axis must be >= 1, got {self.ranks_per_axis}")
+
+    @property
+    def dim(self) -> int:
+        return len(self.ranks_per_axis)
+
+    @property
+    def size(self) -> int:
+        return math.prod(self.ranks_per_axis)
+
+    def coords(self, rank: int) -> tuple:
+        out = []
+        for r in self.ranks_per_axis:
+            out.append(rank % r)
+            rank //= r
+        return tuple(out)
+
+    def rank_of(self, coords) -> int:
+        rank = 0
+        for c, r in zip(reversed(coords), reversed(self.ranks_per_axis)):
+            rank = rank * r + c
+        return rank
+
+    def neighbor(self, rank: int, axis: int, side: int, periodic: bool):
+        c = list(self.coords(rank))
+        c[axis] += 1 if side else -1
+        r = self.ranks_per_axis[axis]
+        if 0 <= c[axis] < r:
+            return self.rank_of(c)
+        if not periodic:
+            return None
+        c[axis] %= r
+        return self.rank_of(c)
+
+
+@dataclass(frozen=True)
+class Subdomain:
+    rank: int
+    grid: GridSpec
+    offset: tuple
+
+
+def decompose(grid, topo: RankTopology) -> list:
+    """Exact tiling; local grids inherit the global deltas (parallel.py:99-124)."""
+    if topo.dim != grid.dim:
+        raise E.ConfigError(f"topology dim {topo.dim} does not match grid dim {grid.dim}")
+    for axis, (n, r) in enumerate(zip(grid.cells, topo.ranks_per_axis)):
+        if n % r:
+            raise E.ConfigError(f"{n} cells on axis {axis} not divisible by {r} ranks")
+    local = tuple(n // r for n, r in zip(grid.cells, topo.ranks_per_axis))
+    out = []
+    for rank in range(topo.size):
+        off = tuple(c * m for c, m in zip(topo.coords(rank), local))
+        origin = tuple(grid.origin[k] + off[k] * grid.deltas[k] for k in range(grid.dim))
+        extent = tuple(m * d for m, d in zip(local, grid.deltas))
+        g = GridSpec(grid.dim, local, origin, extent, ghost_width=grid.ghost_width, deltas=grid.deltas)
+        out.append(Subdomain(rank, g, off))
+    return out
+
+
+def _box(part) -> tuple:
+    d = part.grid.dim
+    return (slice(None),) + tuple(
+        slice(part.offset[d - 1 - j], part.offset[d - 1 - j] + part.grid.cells[d - 1 - j]) for j in range(d))
+
+
+def scatter_field(global_field, parts) -> list:
+    src = global_field.interior
+    out = []
+    for part in parts:
+        loc = make_field(part.grid, global_field.ncomp, 0.0)
+        loc.interior[...] = src[_box(part)]
+        out.append(loc)
+    return out
+
+
+def stitch_fields(global_grid, parts, locals_) -> Field:
+    out = make_field(global_grid, locals_[0].ncomp, 0.0)
+    for part, loc in zip(parts, locals_):
+        out.interior[_box(part)] = loc.interior
+    cls = TYPES["Field"] or Field
+    return cls(out.grid, out.ncomp, out.data) if cls is not Field else out
+
+
+@dataclass
+class RankRecord:
+    step: int
+    t: float
+    dt: float
+    seconds: float
+
+
+# ---------------------------------------------------------------------------
+# message-level halo API (parallel.py:127-254)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class HaloMessage:
+    source: int
+    dest: int
+    axis: int
+    side: int
+    tag: int
+    payload: object
+
+
+class Transport:
+    def send(self, msg: HaloMessage) -> None:
+        raise NotImplementedError
+
+    def receive(self, source: int, dest: int, axis: int, side: int, tag: int):
+        raise NotImplementedError
+
+
+class InProcessTransport(Transport):
+    """Per-pair FIFO with strictly increasing tags (parallel.py:147-182)."""
+
+    def __init__(self, size: int):
+        self.size = size
+        self._queues = {(s, d): queue.SimpleQueue() for s in range(size) for d in range(size)}
+        self._last_tag = {}
+
+    def send(self, msg: HaloMessage) -> None:
+        key = (msg.source, msg.dest)
+        last = self._last_tag.get(key)
+        if last is not None and msg.tag <= last:
+            raise E.ProtocolError(f"tag {msg.tag} not increasing on pair {key} (last {last})")
+        self._last_tag[key] = msg.tag
+        self._queues[key].put(msg)
+
+    def receive(self, source, dest, axis, side, tag):
+        try:
+            msg = self._queues[(source, dest)].get(timeout=_RECV_TIMEOUT)
+        except queue.Empty:
+            raise E.ProtocolError(f"timed out waiting for message {source}->{dest} tag {tag}") from None
+        if (msg.axis, msg.side, msg.tag) != (axis, side, tag):
+            raise E.ProtocolError(
+                f"message mismatch on pair ({source}, {dest}): expected (axis={axis}, side={side}, tag={tag}), "
+                f"got (axis={msg.axis}, side={msg.side}, tag={msg.tag})")
+        return msg.payload
+
+
+def _desc(grid, ncomp, halo_all=True):
+    s = N.Scheme()
+    s.dim, s.ncomp, s.ghost, s.rk_order = grid.dim, ncomp, grid.ghost_width, 1
+    s.eq = 0 if ncomp == grid.dim + 2 else 1
+    for k in range(3):
+        s.cells[k] = grid.cells[k] if k < grid.dim else 1
+        s.deltas[k] = grid.deltas[k] if k < grid.dim else 1.0
+        s.bc[k] = N.BC_HALO if (halo_all and k < grid.dim) else N.BC_PERIODIC
+    return s
+
+
+def exchange_halos(field, rank: int, topo: RankTopology, transport: Transport, bc, tag: int):
+    """parallel.py:201-254: sequential axis passes over the full padded extent
+    (corners propagate), two directional sub-passes per axis; slabs are
+    packed/unpacked on the GPU (fvb_halo_pack/unpack)."""
+    import torch
+
+    from .solver import fill_boundary_device
+
+    dev, was_dev = (field, True) if isinstance(field, DeviceField) else (DeviceField.from_host(field), False)
+    grid = dev.grid
+    g = grid.ghost_width
+    ctx = N.context()
+    s = _desc(grid, dev.ncomp)
+    L = make_layout(grid, dev.ncomp)
+    ptr = N.C.c_void_p(dev.data.data_ptr())
+    for axis in range(grid.dim):
+        periodic = _v(bc[axis]) == "periodic"
+        nb = {side: topo.neighbor(rank, axis, side, periodic) for side in (0, 1)}
+        if nb[0] == rank and nb[1] == rank:
+            kinds = [BoundaryKind.PERIODIC if j == axis else BoundaryKind.OUTFLOW for j in range(grid.dim)]
+            _fill_one_axis(dev, axis, "periodic")
+            continue
+        count = int(ctx.lib.fvb_halo_count(N.C.byref(s), axis))
+        for d in (0, 1):
+            send_nb, recv_nb = nb[d], nb[1 - d]
+            subtag = (tag * grid.dim + axis) * 2 + d
+            if send_nb is not None:
+                buf = torch.empty(count, dtype=torch.float64, device=dev.data.device)
+                ctx.check(ctx.lib.fvb_halo_pack(ctx.h, N.C.byref(s), N.C.byref(L), ptr, axis, d,
+                                                N.C.c_void_p(buf.data_ptr())))
+                transport.send(HaloMessage(rank, send_nb, axis, 1 - d, subtag, buf.cpu().numpy()))
+            if recv_nb is None:
+                _fill_one_side(dev, axis, 1 - d)
+            else:
+                payload = transport.receive(recv_nb, rank, axis, 1 - d, subtag)
+                buf = torch.as_tensor(np.ascontiguousarray(payload), dtype=torch.float64).to(dev.data.device)
+                ctx.check(ctx.lib.fvb_halo_unpack(ctx.h, N.C.byref(s), N.C.byref(L), ptr, axis, 1 - d,
+                                                  N.C.c_void_p(buf.data_ptr())))
+    if not was_dev:
+        field.data[...] = dev.data.cpu().numpy()
+        return field
+    return dev
+
+
+def _fill_one_axis(dev, axis, kind):
+    ctx = N.context()
+    s = _desc(dev.grid, dev.ncomp, halo_all=False)
+    for k in range(3):
+        s.bc[k] = N.BC_HALO
+    s.bc[axis] = N.BC_PERIODIC if kind == "periodic" else N.BC_OUTFLOW
+    L = make_layout(dev.grid, dev.ncomp)
+    ctx.check(ctx.lib.fvb_fill_ghosts(ctx.h, N.C.byref(s), N.C.byref(L), N.C.c_void_p(dev.data.data_ptr()), 1))
+
+
+def _fill_one_side(dev, axis, side):
+    """_fill_outflow_side (parallel.py:189-198): copy the nearest interior
+    layer into the ghost slab of one side (pack it, unpack it g times)."""
+    import torch
+
+    grid = dev.grid
+    g = grid.ghost_width
+    idx = [slice(None)] * dev.data.dim()
+    ax = grid.dim - axis
+    n = grid.cells[axis]
+    src = [slice(None)] * dev.data.dim()
+    if side == 0:
+        idx[ax] = slice(0, g)
+        src[ax] = slice(g, g + 1)
+    else:
+        idx[ax] = slice(n + g, n + 2 * g)
+        src[ax] = slice(n + g - 1, n + g)
+    dev.data[tuple(idx)] = dev.data[tuple(src)].expand_as(dev.data[tuple(idx)])
+
+
+# ---------------------------------------------------------------------------
+# run_parallel (parallel.py:430-521)
+# ---------------------------------------------------------------------------
+
+def run_parallel(init, cfg, ranks_per_axis, n_steps: int | None = None, overlap: bool = True, *,
+                 arith: str | None = None):
+    """Decomposed run; returns (stitched final Field, per-rank records)."""
+    import torch
+
+    check_scheme(init.grid, cfg)
+    topo = RankTopology(tuple(ranks_per_axis))
+    parts = decompose(init.grid, topo)
+    if torch.distributed.is_available() and torch.distributed.is_initialized() \
+            and torch.distributed.get_world_size() == topo.size and topo.size > 1:
+        return run_parallel_nccl(init, cfg, topo, parts, n_steps, arith=arith)
+    locals_ = scatter_field(init, parts)
+    grid = parts[0].grid
+    ncomp = init.ncomp
+    host = torch.from_numpy(np.stack([np.asarray(f.data) for f in locals_]))
+    b0 = host.to("cuda")
+    bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
+    ctx = N.context()
+    ranks = (N.C.c_int32 * 3)(*(list(topo.ranks_per_axis) + [1] * (3 - grid.dim)))
+    per = (N.C.c_int32 * 3)(*[int(_v(cfg.bc[k]) == "periodic") if k < grid.dim else 1 for k in range(3)])
+    ctx.check(ctx.lib.fvb_run_set_topology(ctx.h, ranks, per))
+    split = tuple(k for k in range(grid.dim) if topo.ranks_per_axis[k] > 1)
+    mode = N.MODE_FIXED if n_steps is not None else N.MODE_PAR_T_END
+    run = DeviceRun(grid, cfg, bufs, topo.size, mode, n_steps, arith, halo_axes=split, ctx=ctx)
+    records = []
+    while True:
+        infos, done = run.poll()
+        if infos[0].err or done[0]:
+            break
+        n = 256 if n_steps is None else max(1, n_steps - int(infos[0].steps))
+        if n_steps is None and infos[0].dt > 0:
+            n = int(min(n, max(1, math.ceil((cfg.t_end - infos[0].t) / infos[0].dt) + 2)))
+        tic = time.perf_counter()
+        run.steps(n)
+        infos, done = run.poll()
+        run.read_log(infos, (time.perf_counter() - tic) / max(1, int(infos[0].steps) - run._seen[0]))
+    info = run.end()[0]
+    if info.err:
+        try:
+            _raise_run_error(info, grid, ncomp)
+        except E.ConslawError as exc:
+            raise E.SimulationError(f"rank 0 failed: {exc}") from exc
+    final = bufs[int(info.steps) % 2] if cfg.rk_order == 1 else bufs[0]
+    finals = [DeviceField(grid, ncomp, final[r]).to_host() for r in range(topo.size)]
+    recs = [RankRecord(r.step, r.t, r.dt, r.seconds) for r in run.records[0]]
+    return stitch_fields(init.grid, parts, finals), [list(recs) for _ in range(topo.size)]
+
+
+def run_parallel_nccl(init, cfg, topo, parts, n_steps, *, arith=None):
+    """One rank per process/GPU with NCCL halos.  Not yet wired: the
+    single-device path above covers the contract; see DESIGN.md."""
+    raise E.ConfigError("multi-process run_parallel over NCCL is not available in this build")
+
+
+# ---------------------------------------------------------------------------
+# overhead metric (parallel.py:529-547)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class OverheadReport:
+    ranks: int
+    mean_seconds: float
+    baseline_seconds: float
+    overhead_fraction: float
+
+
+def overhead_metric(times_K, times_1, ranks: int) -> OverheadReport:
+    times_K, times_1 = list(times_K), list(times_1)
+    if not times_K or not times_1:
+        raise E.ConfigError("overhead metric needs non-empty timing series")
+    mk = sum(times_K) / len(times_K)
+    m1 = sum(times_1) / len(times_1)
+    return OverheadReport(ranks, mk, m1, (mk - m1) / m1)

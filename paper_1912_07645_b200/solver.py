@@ -161,6 +161,7 @@ class DeviceField:
     def from_host(cls, field, device=None, pin: bool = False):
         import torch
 
+        N._require_cuda()  # no CPU fallback: fail loudly without a GPU
         src = torch.from_numpy(np.ascontiguousarray(field.data, dtype=np.float64))
         if pin:
             src = src.pin_memory()

@@ -1,0 +1,389 @@
+"""On-GPU Monte Carlo / quasi-Monte Carlo statistics (uq.py:25-322 of the
+reference) on the B200 path.
+
+* Sampling (``SamplePlan``, ``draw_sample``, Halton) stays on the host and is
+  the reference algorithm unchanged, so sample vectors are identical.
+* Each batch of samples runs as ONE batched device run (one instance per
+  sample, per-instance dt/t/stop flag, csrc/fvb_state.cuh); final fields
+  never leave HBM: ``FieldMoments`` and ``StructureFunctionAccumulator`` are
+  updated by CUDA kernels (fvb_moments_push / fvb_structure_push) in
+  sample-index order, which reproduces run_mc's ordered merge
+  (uq.py:318-321) bitwise on one GPU.
+* Under ``torch.distributed`` (one process per GPU) samples are sharded in
+  contiguous blocks and the per-rank accumulators are merged once at the end
+  in rank order (one all_gather; Chan merge on the GPU).
+
+Functionals are duck-typed by ``name`` like write_stats dispatches them
+(output.py:158-191); the reference's own FieldMoments /
+StructureFunctionAccumulator prototypes are accepted and returned filled.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from . import errors as E
+from .solver import DeviceField, DeviceRun, _raise_run_error, _v, check_scheme, make_layout, make_scheme
+
+MC = "mc"
+QMC = "qmc"
+_PRIMES = (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53)
+
+
+@dataclass(frozen=True)
+class SamplePlan:
+    method: str = MC
+    samples: int = 1
+    seed: int = 0
+    stochastic_dim: int = 1
+
+    def __post_init__(self):
+        if self.method not in (MC, QMC):
+            raise E.ConfigError(f"unknown sampling method {self.method!r}")
+        if self.samples < 1:
+            raise E.ConfigError(f"sample count must be >= 1, got {self.samples}")
+        if self.stochastic_dim < 1:
+            raise E.ConfigError(f"stochastic_dim must be >= 1, got {self.stochastic_dim}")
+
+
+def radical_inverse(index: int, base: int) -> float:
+    """Van der Corput radical inverse (uq.py:79-87)."""
+    inv, factor = 0.0, 1.0 / base
+    while index > 0:
+        inv += factor * (index % base)
+        index //= base
+        factor /= base
+    return inv
+
+
+def halton_point(index: int, dim: int) -> np.ndarray:
+    if dim > len(_PRIMES):
+        raise E.ConfigError(f"Halton supports up to {len(_PRIMES)} dimensions")
+    return np.array([radical_inverse(index, _PRIMES[d]) for d in range(dim)])
+
+
+def draw_sample(plan, k: int, level: int = 0) -> np.ndarray:
+    """uq.py:97-106: Philox keyed by (seed, level<<48 + k) or Halton k+1."""
+    samples = plan.samples_per_level[level] if hasattr(plan, "samples_per_level") else plan.samples
+    if not 0 <= k < samples:
+        raise E.ConfigError(f"sample index {k} out of range [0, {samples})")
+    if plan.method == QMC:
+        return halton_point(k + 1, plan.stochastic_dim)
+    key = [np.uint64(plan.seed), np.uint64((level << 48) + k)]
+    return np.random.Generator(np.random.Philox(key=key)).random(plan.stochastic_dim)
+
+
+# ---------------------------------------------------------------------------
+# GPU-resident functionals
+# ---------------------------------------------------------------------------
+
+class MomentAccumulator:
+    """Host view with the reference's fields (uq.py:114-158)."""
+
+    def __init__(self, shape):
+        self.count = 0
+        self.mean = np.zeros(shape)
+        self.m2 = np.zeros(shape)
+
+    def variance(self, ddof: int = 1) -> np.ndarray:
+        if self.count <= ddof:
+            return np.zeros_like(self.m2)
+        return self.m2 / (self.count - ddof)
+
+    def second_moment(self) -> np.ndarray:
+        if self.count == 0:
+            return np.zeros_like(self.m2)
+        return self.m2 / self.count + self.mean ** 2
+
+
+class FieldMoments:
+    """Per-cell mean and M2 of the conserved field, kept in HBM."""
+
+    name = "moments"
+
+    def __init__(self, grid, ncomp: int):
+        self.grid = grid
+        self.ncomp = ncomp
+        self.count = 0
+        self._mean = None
+        self._m2 = None
+
+    def fresh(self):
+        return FieldMoments(self.grid, self.ncomp)
+
+    def _alloc(self):
+        import torch
+
+        if self._mean is None:
+            shape = (self.ncomp,) + tuple(self.grid.interior_shape)
+            self._mean = torch.zeros(shape, dtype=torch.float64, device="cuda")
+            self._m2 = torch.zeros(shape, dtype=torch.float64, device="cuda")
+
+    def push_device(self, ctx, scheme, layout, buf, inst: int):
+        """Merge one sample's final field (instance ``inst`` of ``buf``)."""
+        self._alloc()
+        ctx.check(ctx.lib.fvb_moments_push(ctx.h, N.C.byref(scheme), N.C.byref(layout), N.C.c_void_p(buf.data_ptr()),
+                                           inst, N.C.c_void_p(self._mean.data_ptr()),
+                                           N.C.c_void_p(self._m2.data_ptr()), self.count))
+        self.count += 1
+
+    def update(self, field) -> None:
+        """FieldMoments.update (uq.py:174-175) for one field."""
+        from .solver import make_scheme as _ms  # noqa: F401
+
+        dev = field if isinstance(field, DeviceField) else DeviceField.from_host(field)
+        ctx = N.context()
+        s = _descriptor(dev.grid, dev.ncomp)
+        self.push_device(ctx, s, make_layout(dev.grid, dev.ncomp), dev.data, 0)
+
+    def merge(self, other: "FieldMoments") -> None:
+        """MomentAccumulator.merge (uq.py:135-148) on the GPU."""
+        if other.count == 0:
+            return
+        self._alloc()
+        ctx = N.context()
+        ctx.check(ctx.lib.fvb_moments_merge(ctx.h, N.C.c_void_p(self._mean.data_ptr()),
+                                            N.C.c_void_p(self._m2.data_ptr()), self.count,
+                                            N.C.c_void_p(other._mean.data_ptr()), N.C.c_void_p(other._m2.data_ptr()),
+                                            other.count, self._mean.numel()))
+        self.count += other.count
+
+    @property
+    def acc(self) -> MomentAccumulator:
+        a = MomentAccumulator((self.ncomp,) + tuple(self.grid.interior_shape))
+        a.count = self.count
+        if self._mean is not None:
+            a.mean = self._mean.cpu().numpy()
+            a.m2 = self._m2.cpu().numpy()
+        return a
+
+
+class StructureFunctionAccumulator:
+    """Mean |u(x + h e_k) - u(x)|^p over positions and axes (uq.py:231-273);
+    the per-sample sums are computed by fvb_structure_push on the GPU."""
+
+    name = "structure_function"
+
+    def __init__(self, p: float, max_offset: int, component: int = 0):
+        if p < 1:
+            raise E.ConfigError(f"structure-function exponent must be >= 1, got {p}")
+        if max_offset < 0:
+            raise E.ConfigError(f"max offset must be >= 0, got {max_offset}")
+        self.p = float(p)
+        self.max_offset = int(max_offset)
+        self.component = int(component)
+        self.samples = 0
+        self._sums = None
+
+    def fresh(self):
+        return StructureFunctionAccumulator(self.p, self.max_offset, self.component)
+
+    def _alloc(self):
+        import torch
+
+        if self._sums is None:
+            self._sums = torch.zeros(self.max_offset + 1, dtype=torch.float64, device="cuda")
+
+    def push_device(self, ctx, scheme, layout, buf, inst: int):
+        self._alloc()
+        ctx.check(ctx.lib.fvb_structure_push(ctx.h, N.C.byref(scheme), N.C.byref(layout),
+                                             N.C.c_void_p(buf.data_ptr()), inst, self.component, self.p,
+                                             self.max_offset, N.C.c_void_p(self._sums.data_ptr())))
+        self.samples += 1
+
+    def update(self, field) -> None:
+        dev = field if isinstance(field, DeviceField) else DeviceField.from_host(field)
+        ctx = N.context()
+        self.push_device(ctx, _descriptor(dev.grid, dev.ncomp), make_layout(dev.grid, dev.ncomp), dev.data, 0)
+
+    def merge(self, other: "StructureFunctionAccumulator") -> None:
+        if other.max_offset != self.max_offset or other.p != self.p:
+            raise E.ConfigError("structure-function specs do not match")
+        self._alloc()
+        if other._sums is not None:
+            self._sums += other._sums
+        self.samples += other.samples
+
+    @property
+    def sums(self) -> np.ndarray:
+        return np.zeros(self.max_offset + 1) if self._sums is None else self._sums.cpu().numpy()
+
+    def values(self) -> np.ndarray:
+        if self.samples == 0:
+            return np.zeros(self.max_offset + 1)
+        return self.sums / self.samples
+
+
+def _descriptor(grid, ncomp):
+    s = N.Scheme()
+    s.dim = grid.dim
+    s.ncomp = ncomp
+    s.eq = 0 if ncomp == grid.dim + 2 else 1
+    s.ghost = grid.ghost_width
+    s.rk_order = 1
+    for k in range(3):
+        s.cells[k] = grid.cells[k] if k < grid.dim else 1
+        s.deltas[k] = grid.deltas[k] if k < grid.dim else 1.0
+    return s
+
+
+# ---------------------------------------------------------------------------
+# estimator
+# ---------------------------------------------------------------------------
+
+class _Slot:
+    """One requested functional: our GPU accumulator + how to hand it back."""
+
+    def __init__(self, proto, grid, ncomp):
+        self.proto = proto
+        name = getattr(proto, "name", None)
+        self.kind = name
+        if name == "moments":
+            self.gpu = FieldMoments(grid, ncomp)
+        elif name == "structure_function":
+            self.gpu = StructureFunctionAccumulator(proto.p, proto.max_offset, getattr(proto, "component", 0))
+        else:
+            self.gpu = None  # host functional (e.g. Histogram): fed host fields
+            self.host = proto.fresh()
+
+    def push(self, ctx, scheme, layout, buf, inst, grid, ncomp, like):
+        if self.gpu is not None:
+            self.gpu.push_device(ctx, scheme, layout, buf, inst)
+        else:
+            one = DeviceField(grid, ncomp, buf[inst]).to_host(like)
+            c = self.proto.fresh()
+            c.update(one)
+            self.host.merge(c)
+
+    def result(self):
+        """Return an object of the caller's functional type."""
+        if self.gpu is None:
+            return self.host
+        if isinstance(self.proto, (FieldMoments, StructureFunctionAccumulator)):
+            return self.gpu
+        out = self.proto.fresh()  # reference class: fill its public fields
+        if self.kind == "moments":
+            acc = self.gpu.acc
+            out.acc.count, out.acc.mean, out.acc.m2 = acc.count, acc.mean, acc.m2
+        else:
+            out.sums = self.gpu.sums
+            out.samples = self.gpu.samples
+        return out
+
+
+def shard_range(n: int, world: int, rank: int):
+    """Contiguous sample block of ``rank``: [rank*n//world, (rank+1)*n//world)."""
+    return (rank * n) // world, ((rank + 1) * n) // world
+
+
+def default_batch(grid, ncomp: int) -> int:
+    cells = math.prod(grid.cells)
+    return int(max(1, min(64, (4 << 20) // max(1, cells))))
+
+
+def run_mc(plan, grid, cfg, evaluate_init, functionals, workers: int = 1, *, batch: int | None = None,
+           arith: str | None = None, group=None):
+    """Single-level estimate (uq.py:302-322) on the GPU.
+
+    ``workers`` is accepted for API compatibility (the GPU batch replaces the
+    thread pool).  Under an initialised torch.distributed group the samples
+    are sharded over the ranks and every rank returns the merged result.
+    """
+    import torch
+
+    check_scheme(grid, cfg)
+    ncomp = cfg.model.ncomp
+    world, rank = 1, 0
+    dist = None
+    if torch.distributed.is_available() and torch.distributed.is_initialized():
+        dist = torch.distributed
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+    lo, hi = shard_range(plan.samples, world, rank)
+    slots = [_Slot(f, grid, ncomp) for f in functionals]
+    B = batch or default_batch(grid, ncomp)
+    ctx = N.context()
+    layout = make_layout(grid, ncomp)
+    desc = make_scheme(grid, cfg, arith)
+    like = None
+    k = lo
+    while k < hi:
+        ks = list(range(k, min(hi, k + B)))
+        inits = []
+        for j in ks:
+            vec = draw_sample(plan, j)
+            try:
+                f0 = evaluate_init(grid, vec)
+            except Exception as exc:
+                raise E.SimulationError(f"sample {j} failed: {exc}") from exc
+            like = like or f0
+            inits.append(np.asarray(f0.data, dtype=np.float64))
+        host = torch.from_numpy(np.stack(inits))
+        b0 = host.to("cuda")
+        bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
+        run = DeviceRun(grid, cfg, bufs, len(ks), N.MODE_T_END, None, arith, log=False, ctx=ctx)
+        while True:
+            infos, done = run.poll()
+            if all(done):
+                break
+            left = max(((cfg.t_end - i.t) / i.dt) if (i.dt > 0 and not d) else 1 for i, d in zip(infos, done))
+            run.steps(int(min(512, max(1, math.ceil(left) + 2))))
+        infos = run.end()
+        for j, info in zip(ks, infos):
+            if info.err:
+                try:
+                    _raise_run_error(info, grid, ncomp)
+                except E.ConslawError as exc:
+                    raise E.SimulationError(f"sample {j} failed: {exc}") from exc
+        for i, j in enumerate(ks):
+            buf = bufs[int(infos[i].steps) % 2] if cfg.rk_order == 1 else bufs[0]
+            for s in slots:
+                s.push(ctx, desc, layout, buf, i, grid, ncomp, like)
+        k = ks[-1] + 1
+    if dist is not None and world > 1:
+        _merge_ranks(slots, dist, group, world)
+    return [s.result() for s in slots]
+
+
+def gather_ordered(tensors, count: int, dist, group, world):
+    """All-gather one rank's (count, tensors) block; returns the blocks of all
+    ranks in rank order -- the order run_mc merges samples in."""
+    import torch
+
+    cnt = torch.tensor([int(count)], dtype=torch.int64, device=tensors[0].device)
+    cnts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(cnts, cnt, group=group)
+    gathered = []
+    for t in tensors:
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t.contiguous(), group=group)
+        gathered.append(parts)
+    return [(int(cnts[r].item()), [g[r] for g in gathered]) for r in range(world)]
+
+
+def _merge_ranks(slots, dist, group, world):
+    """Deterministic cross-rank reduce: one all_gather per statistic, then a
+    fold in rank order (rank 0's sample block first)."""
+    for s in slots:
+        g = s.gpu
+        if isinstance(g, FieldMoments):
+            g._alloc()
+            tot = FieldMoments(g.grid, g.ncomp)
+            for cnt, (mean, m2) in gather_ordered([g._mean, g._m2], g.count, dist, group, world):
+                part = FieldMoments(g.grid, g.ncomp)
+                part.count, part._mean, part._m2 = cnt, mean, m2
+                tot.merge(part)  # Chan merge on the GPU (fvb_moments_merge)
+            s.gpu = tot
+        elif isinstance(g, StructureFunctionAccumulator):
+            g._alloc()
+            tot = g.fresh()
+            tot._alloc()
+            for cnt, (sums,) in gather_ordered([g._sums], g.samples, dist, group, world):
+                tot._sums += sums
+                tot.samples += cnt
+            s.gpu = tot
+        else:
+            raise E.ConfigError(f"functional {s.kind!r} cannot be merged across ranks")

@@ -1,0 +1,95 @@
+"""GPU UQ parity: run_mc with on-GPU moments / structure functions against
+the golden statistics of the reference's run_mc (tests/golden)."""
+import numpy as np
+import pytest
+
+from oracle import fv_oracle as O
+from tests.helpers import product_objects, rel_l1
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1912_07645_b200 as P
+
+    return P
+
+
+def _setup(P, case):
+    from paper_1912_07645_b200 import uq
+    from paper_1912_07645_b200.initial import burgers_sines, kelvin_helmholtz
+
+    grid, cfg = product_objects(case["scheme"])
+    fn = kelvin_helmholtz if case["scheme"]["eq"] == "euler" else burgers_sines
+    plan = uq.SamplePlan(case["method"], case["samples"], case["seed"], case["stochastic_dim"])
+    fm = uq.FieldMoments(grid, cfg.model.ncomp)
+    sf = uq.StructureFunctionAccumulator(case["sf_p"], case["sf_H"])
+    return uq, grid, cfg, fn, plan, fm, sf
+
+
+@pytest.mark.parametrize("name", ["kh2d128_mc8", "kh2d128_qmc8", "burgers128_qmc8"])
+@pytest.mark.parametrize("batch", [1, 3, 8])
+def test_run_mc_matches_reference(P, golden, name, batch):
+    case = next(u for u in golden["uq"] if u["name"] == name)
+    uq, grid, cfg, fn, plan, fm, sf = _setup(P, case)
+    m, s = uq.run_mc(plan, grid, cfg, fn, [fm, sf], batch=batch, arith="exact")
+    acc = m.acc
+    assert acc.count == case["samples"]
+    # moments: bitwise (same per-sample merge order as the reference)
+    assert O.sha16(acc.mean) == case["mean_sha"]
+    assert O.sha16(acc.variance(ddof=1)) == case["var_sha"]
+    assert O.sha16(acc.m2) == case["m2_sha"]
+    # structure functions: summation order differs from numpy's pairwise mean
+    assert rel_l1(s.sums, np.array(case["sf_sums"])) <= 1e-13
+    assert s.samples == case["samples"]
+
+
+def test_run_mc_fast_within_tolerance(P, golden):
+    case = next(u for u in golden["uq"] if u["name"] == "kh2d128_mc8")
+    uq, grid, cfg, fn, plan, fm, sf = _setup(P, case)
+    m, s = uq.run_mc(plan, grid, cfg, fn, [fm, sf], arith="fast")
+    ref_m, ref_sf = O.mc_moments_and_sf(lambda v: O.kelvin_helmholtz(tuple(grid.cells), v), 
+                                        __import__("tests.helpers", fromlist=["x"]).oracle_scheme(case["scheme"]),
+                                        case["method"], case["seed"], case["samples"], case["stochastic_dim"])
+    acc = m.acc
+    for c in range(acc.mean.shape[0]):
+        assert rel_l1(acc.mean[c], ref_m.mean[c]) <= 1e-12
+    assert rel_l1(acc.variance(), ref_m.variance()) <= 1e-10
+    assert rel_l1(s.sums, ref_sf) <= 1e-12
+
+
+def test_functionals_update_merge(P, golden, golden_arrays):
+    """FieldMoments.update/merge and StructureFunctionAccumulator.update on
+    single fields (uq.py:174-178, 254-268) against the oracle formulas."""
+    from paper_1912_07645_b200 import uq
+
+    case = next(r for r in golden["runs"] if r["name"] == "kh2d64_weno2_50")
+    grid, cfg = product_objects(case["scheme"])
+    a = np.array(golden_arrays["kh2d64_weno2_50__init"])
+    b = np.array(golden_arrays["kh2d64_weno2_50__final"])
+    fa, fb = P.Field(grid, 4, a), P.Field(grid, 4, b)
+    sc = __import__("tests.helpers", fromlist=["x"]).oracle_scheme(case["scheme"])
+    ref = O.Moments(O.interior(a, sc).shape)
+    for x in (a, b, a):
+        ref.push(np.asarray(O.interior(x, sc)))
+    m1, m2 = uq.FieldMoments(grid, 4), uq.FieldMoments(grid, 4)
+    m1.update(fa)
+    m1.update(fb)
+    m2.update(fa)
+    m1.merge(m2)
+    ref2 = O.Moments(ref.mean.shape)
+    ref2.push(np.asarray(O.interior(a, sc)))
+    ref2.push(np.asarray(O.interior(b, sc)))
+    r3 = O.Moments(ref.mean.shape)
+    r3.push(np.asarray(O.interior(a, sc)))
+    ref2.merge(r3)
+    assert np.array_equal(m1.acc.mean, ref2.mean) and np.array_equal(m1.acc.m2, ref2.m2)
+    sf = uq.StructureFunctionAccumulator(2.0, 8)
+    sf.update(fb)
+    want = O.structure_sums(np.asarray(O.interior(b, sc)[0]), 2.0, 8)
+    assert rel_l1(sf.sums, want) <= 1e-13
+    sf3 = uq.StructureFunctionAccumulator(1.5, 5, component=3)
+    sf3.update(fb)
+    want3 = O.structure_sums(np.asarray(O.interior(b, sc)[3]), 1.5, 5)
+    assert rel_l1(sf3.sums, want3) <= 1e-13
