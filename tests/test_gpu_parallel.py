@@ -36,8 +36,8 @@ def test_run_parallel_fixed_bitwise(P, golden, golden_arrays, name, layouts):
 
     case = next(r for r in golden["runs"] if r["name"] == name)
     grid, cfg = product_objects(case["scheme"])
-    init = P.Field(grid, 0, np.array(golden_arrays[name + "__init"]))
-    init.ncomp = init.data.shape[0]
+    data = np.array(golden_arrays[name + "__init"])
+    init = P.Field(grid, data.shape[0], data)
     sc = oracle_scheme(case["scheme"])
     n = 6
     ref, log = O.simulate_fixed(init.data, sc, n)

@@ -187,3 +187,4 @@ def test_fast_mode_divergence_growth(P, golden, golden_arrays, name):
     for m, e, per in rows:
         print(f"{name} steps={m:3d} rel_l1_field={e:.3e} per-component={['%.2e' % x for x in per]}")
     assert rows[0][1] <= 1e-13
+    assert all(e <= TOL_FAST for _, e, _ in rows)
