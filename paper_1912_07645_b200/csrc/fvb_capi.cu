@@ -185,8 +185,13 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst) {
     int64_t ytiles = 1;
     if (s.dim == 3) ytiles = (p.n[1] + (nty - 2) - 1) / (nty - 2);
     // aim for ~2 waves of resident blocks over 148 SMs
-    const int64_t per_sm = s.dim == 3 ? 1 : (p.variant == 0 ? 4 : 6);
-    const int64_t target = 148 * per_sm * 2;
+    // resident blocks per SM (register-limited) and waves of blocks: one
+    // wave keeps the march long (fewer redundant halo rows per chunk)
+    int64_t per_sm = s.dim == 3 ? 1 : (p.variant == 0 ? 4 : 8);
+    int64_t waves = 1;
+    if (const char* e = getenv("FVB_BLOCKS_PER_SM")) per_sm = std::max(1, atoi(e));
+    if (const char* e = getenv("FVB_WAVES")) waves = std::max(1, atoi(e));
+    const int64_t target = 148 * per_sm * waves;
     int64_t want_chunks = (target + strips * ytiles * ninst - 1) / (strips * ytiles * ninst);
     want_chunks = std::max<int64_t>(1, std::min<int64_t>(want_chunks, nm));
     H = (nm + want_chunks - 1) / want_chunks;

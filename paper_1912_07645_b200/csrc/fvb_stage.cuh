@@ -139,40 +139,244 @@ __device__ __forceinline__ void block_epilogue(const StageParams& p, FvbState* s
   }
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory tile kernel (default for 1D/2D, the 3D path).
+//
+// A block of NT (x) [x NTY (y, 3D)] threads owns NT-2 [x NTY-2] cells of the
+// plane and marches H rows along the slowest axis.  Thread <-> "face cell"
+// mapping: every WENO face pair of the plane is computed once per row and
+// every interface flux once (+2/NT halo).  The march axis uses a per-thread
+// 3-row register window; the row loop is unrolled by 3 with the window
+// arrays rotated by NAME (no register moves) and the row after next loaded
+// into the slot that just died.
+// ---------------------------------------------------------------------------
 template <int DIM, int EQ, int FLUX, int RECON, int NT, int NTY>
-__global__ void __launch_bounds__(NT * NTY)
+struct TileCtx {
+  static constexpr int NC = NComp<EQ, DIM>::value;
+  static constexpr bool WENO = RECON != RECON_NONE;
+  static constexpr bool MARCH = DIM >= 2;
+  static constexpr bool PY = DIM == 3;          // y handled in-plane (3D)
+  static constexpr int SUY = PY ? NTY + 2 : 1;  // rows of the plane tile in smem
+  static constexpr int OY = PY ? 1 : 0;
+  static constexpr int MA = DIM - 1;            // march axis
+  static constexpr int nU = NC * SUY * (NT + 2);
+  static constexpr int nFX = WENO ? NC * NTY * NT : 0;
+  static constexpr int nGX = NC * NTY * NT;
+  static constexpr int nFY = (WENO && PY) ? NC * NTY * NT : 0;
+
+  const StageParams& p;
+  FvbState* st;
+  const double* __restrict__ us;
+  const double* un;
+  double* out;
+  double* smem;
+  double dt;
+  int tx, ty;
+  int64_t x0, y0, xf, yf;
+  bool cell;
+  int64_t ra, rb;
+  int64_t co;  // mapped in-plane offset of this thread's column
+  unsigned errb;
+  double smax[DIM];
+
+  __device__ __forceinline__ double& U(int c, int y, int x) const { return smem[(c * SUY + y) * (NT + 2) + x]; }
+  __device__ __forceinline__ double& HX(int c, int y, int x) const { return smem[nU + (c * NTY + y) * NT + x]; }
+  __device__ __forceinline__ double& LX(int c, int y, int x) const { return smem[nU + nFX + (c * NTY + y) * NT + x]; }
+  __device__ __forceinline__ double& GX(int c, int y, int x) const {
+    return smem[nU + 2 * nFX + (c * NTY + y) * NT + x];
+  }
+  __device__ __forceinline__ double& HY(int c, int y, int x) const {
+    return smem[nU + 2 * nFX + nGX + (c * NTY + y) * NT + x];
+  }
+  __device__ __forceinline__ double& LY(int c, int y, int x) const {
+    return smem[nU + 2 * nFX + nGX + nFY + (c * NTY + y) * NT + x];
+  }
+  __device__ __forceinline__ double& GY(int c, int y, int x) const {
+    return smem[nU + 2 * nFX + nGX + 2 * nFY + (c * NTY + y) * NT + x];
+  }
+
+  __device__ __forceinline__ int64_t roff(int64_t r) const {
+    if constexpr (DIM == 2) return map_index(r, p.n[1], p.bc[1], p.g) * p.sy;
+    else if constexpr (DIM == 3) return map_index(r, p.n[2], p.bc[2], p.g) * p.sz;
+    else return 0;
+  }
+  __device__ __forceinline__ int64_t pin(int64_t x, int64_t y) const {
+    int64_t o = map_index(x, p.n[0], p.bc[0], p.g);
+    if constexpr (PY) o += map_index(y, p.n[1], p.bc[1], p.g) * p.sy;
+    return o;
+  }
+  __device__ __forceinline__ void load_col(int64_t r, double* v) const { load_nc<NC>(us, co + roff(r), p.sc, v); }
+
+  __device__ __forceinline__ void finish(int64_t r, const double* usc, const double* unc, const double* Lc) {
+    double v[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) v[c] = rk_combine(p.kind, unc[c], usc[c], dt, Lc[c]);
+    const int64_t o = co + roff(r);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
+    if (p.final_stage) post_cell<EQ, DIM, NC>(p, st, v, xf, PY ? yf : (MARCH ? r : 0), PY ? r : 0, smax);
+  }
+
+  // in-plane axes (x; x and y in 3D) of row r: R <- residual of this cell
+  __device__ __forceinline__ void inplane(int64_t r, const double* B, double* R) {
+    if constexpr (EQ == EQ_EULER) {  // stage-start interior check (solver.py:90-93)
+      if (cell && !euler_physical<DIM>(B, p.P)) {
+        const long long key = ((long long)p.stage_idx << 42) |
+                              flat_cell<DIM>(p, xf, PY ? yf : (MARCH ? r : 0), PY ? r : 0);
+        atomicMin(&st->stage_err, key);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) U(c, ty + OY, tx + 1) = B[c];
+    if constexpr (WENO) {
+      if ((!PY || (ty >= 1 && ty <= NTY - 2)) && (tx == 0 || tx == NT - 1)) {
+        const int64_t hxo = pin(tx == 0 ? x0 - 2 : x0 + NT - 1, yf) + roff(r);
+        const int col = tx == 0 ? 0 : NT + 1;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) U(c, ty + OY, col) = __ldg(us + hxo + c * p.sc);
+      }
+      if constexpr (PY) {
+        if ((ty == 0 || ty == NTY - 1) && tx >= 1 && tx <= NT - 2) {
+          const int64_t hyo = pin(xf, ty == 0 ? y0 - 2 : y0 + NTY - 1) + roff(r);
+          const int row = ty == 0 ? 0 : NTY + 1;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) U(c, row, tx + 1) = __ldg(us + hyo + c * p.sc);
+        }
+      }
+    }
+    __syncthreads();
+    if constexpr (WENO) {
+      if (!PY || (ty >= 1 && ty <= NTY - 2)) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          weno_faces<RECON>(U(c, ty + OY, tx), U(c, ty + OY, tx + 1), U(c, ty + OY, tx + 2), p.P.eps,
+                            HX(c, ty, tx), LX(c, ty, tx));
+      }
+      if constexpr (PY) {
+        if (tx >= 1 && tx <= NT - 2) {
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+            weno_faces<RECON>(U(c, ty, tx + 1), U(c, ty + 1, tx + 1), U(c, ty + 2, tx + 1), p.P.eps,
+                              HY(c, ty, tx), LY(c, ty, tx));
+        }
+      }
+      __syncthreads();
+    }
+    // interface fluxes: x interface tx sits between face cells tx-1 and tx
+    if (tx >= 1 && (!PY || (ty >= 1 && ty <= NTY - 2))) {
+      double uL[NC], uR[NC], cl[NC], cr[NC], G[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        cl[c] = U(c, ty + OY, tx);
+        cr[c] = U(c, ty + OY, tx + 1);
+        if constexpr (WENO) {
+          uL[c] = HX(c, ty, tx - 1);
+          uR[c] = LX(c, ty, tx);
+        } else {
+          uL[c] = cl[c];
+          uR[c] = cr[c];
+        }
+      }
+      unsigned eb = 0;
+      interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 0, p.P, G, eb);
+      if (eb && xf <= p.n[0] && (!PY || yf < p.n[1])) errb |= 1u;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) GX(c, ty, tx) = G[c];
+    }
+    if constexpr (PY) {
+      if (ty >= 1 && tx >= 1 && tx <= NT - 2) {
+        double uL[NC], uR[NC], cl[NC], cr[NC], G[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          cl[c] = U(c, ty, tx + 1);
+          cr[c] = U(c, ty + 1, tx + 1);
+          if constexpr (WENO) {
+            uL[c] = HY(c, ty - 1, tx);
+            uR[c] = LY(c, ty, tx);
+          } else {
+            uL[c] = cl[c];
+            uR[c] = cr[c];
+          }
+        }
+        unsigned eb = 0;
+        interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 1, p.P, G, eb);
+        if (eb && yf <= p.n[1] && xf < p.n[0]) errb |= 2u;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) GY(c, ty, tx) = G[c];
+      }
+    }
+    __syncthreads();
+    if (cell) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+#if FVB_FAST
+        double res = (GX(c, ty, tx) - GX(c, ty, tx + 1)) * p.id[0];
+        if constexpr (PY) res = fma(GY(c, ty, tx) - GY(c, ty + 1, tx), p.id[1], res);
+#else
+        double res = 0.0 - ddiv(GX(c, ty, tx + 1) - GX(c, ty, tx), p, 0);
+        if constexpr (PY) res = res - ddiv(GY(c, ty + 1, tx) - GY(c, ty, tx), p, 1);
+#endif
+        R[c] = res;
+      }
+    }
+  }
+
+  // One march row r.  On entry A,B,C = u[r-1], u[r], u[r+1]; on exit A
+  // holds u[r+2].  H: high march-face of row r-1 -> r; G: march flux
+  // (r-2|r-1) -> (r-1|r); R: in-plane residual of row r-1 -> r.
+  __device__ __forceinline__ void row(int64_t r, double* A, const double* B, const double* C, double* H, double* G,
+                                      double* R) {
+    const bool fin = cell && r - 1 >= ra;
+    double unc[NC];
+    if (fin && p.kind >= 2) {
+      const int64_t o = co + roff(r - 1);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) unc[c] = un[o + c * p.sc];
+    }
+    if (cell) {
+      double hi[NC], lo[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) weno_faces<RECON>(A[c], B[c], C[c], p.P.eps, hi[c], lo[c]);
+      if (r >= ra) {
+        double GC[NC];
+        unsigned eb = 0;
+        interface_flux<EQ, FLUX, DIM, RECON>(H, lo, A, B, MA, p.P, GC, eb);
+        if (eb) errb |= 1u << MA;
+        if (fin) {
+          double Lc[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+#if FVB_FAST
+            Lc[c] = fma(G[c] - GC[c], p.id[MA], R[c]);
+#else
+            Lc[c] = R[c] - ddiv(GC[c] - G[c], p, MA);
+#endif
+          }
+          finish(r - 1, A, unc, Lc);
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) G[c] = GC[c];
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) H[c] = hi[c];
+    }
+    if (r + 2 <= rb + 1) load_col(r + 2, A);  // A is dead: the row after next
+    if (r >= ra && r < rb) inplane(r, B, R);
+  }
+};
+
+#ifndef FVB_TILE_MINB
+#define FVB_TILE_MINB 8  // 2D: cap at 128 registers -> 16 warps/SM (measured best)
+#endif
+#ifndef FVB_TILE_UNROLL
+#define FVB_TILE_UNROLL 1
+#endif
+template <int DIM, int EQ, int FLUX, int RECON, int NT, int NTY>
+__global__ void __launch_bounds__(NT * NTY, (DIM == 2 ? FVB_TILE_MINB : 1))
 stage_kernel(const StageParams p) {
-  constexpr int NC = NComp<EQ, DIM>::value;
-  constexpr bool WENO = RECON != RECON_NONE;
-  constexpr bool MARCH = DIM >= 2;
-  constexpr bool PY = DIM == 3;          // y handled in-plane (3D)
-  constexpr int SUY = PY ? NTY + 2 : 1;  // rows of the plane tile in smem
-  constexpr int OY = PY ? 1 : 0;
-  constexpr int MA = DIM - 1;            // march axis
-
-  // shared-memory carve-up (dynamic: the 3D Euler tile exceeds 48 KB)
+  using T = TileCtx<DIM, EQ, FLUX, RECON, NT, NTY>;
+  constexpr int NC = T::NC;
   extern __shared__ double smem[];
-  constexpr int nU = NC * SUY * (NT + 2);
-  constexpr int nFX = WENO ? NC * NTY * NT : 0;
-  constexpr int nGX = NC * NTY * NT;
-  constexpr int nFY = (WENO && PY) ? NC * NTY * NT : 0;
-  double* const pU = smem;
-  double* const pHx = pU + nU;
-  double* const pLx = pHx + nFX;
-  double* const pGx = pLx + nFX;
-  double* const pHy = pGx + nGX;
-  double* const pLy = pHy + nFY;
-  double* const pGy = pLy + nFY;
-#define sU(c, y, x) pU[((c) * SUY + (y)) * (NT + 2) + (x)]
-#define sHx(c, y, x) pHx[((c) * NTY + (y)) * NT + (x)]
-#define sLx(c, y, x) pLx[((c) * NTY + (y)) * NT + (x)]
-#define sGx(c, y, x) pGx[((c) * NTY + (y)) * NT + (x)]
-#define sHy(c, y, x) pHy[((c) * NTY + (y)) * NT + (x)]
-#define sLy(c, y, x) pLy[((c) * NTY + (y)) * NT + (x)]
-#define sGy(c, y, x) pGy[((c) * NTY + (y)) * NT + (x)]
-
-  const int tx = threadIdx.x;
-  const int ty = PY ? threadIdx.y : 0;
   int inst, chunk;
   int64_t y0 = 0;
   if constexpr (DIM == 3) {
@@ -188,235 +392,70 @@ stage_kernel(const StageParams p) {
   }
   FvbState* st = p.st + (p.shared_state ? 0 : inst);
   if (*(volatile int*)&st->done) return;  // uniform over the block
-  const double dt = p.kind == 0 ? 0.0 : *(volatile double*)&st->dt;
-
-  const double* __restrict__ us = p.us + p.origin + inst * p.si;
-  const double* un = p.un + p.origin + inst * p.si;
-  double* out = p.out + p.origin + inst * p.si;
-
-  const int64_t nx = p.n[0], ny = p.n[1];
+  const int tx = threadIdx.x;
+  const int ty = T::PY ? threadIdx.y : 0;
   const int64_t x0 = (int64_t)blockIdx.x * (NT - 2);
   const int64_t xf = x0 - 1 + tx;
-  const int64_t yf = PY ? y0 - 1 + ty : 0;
-  bool cell = tx >= 1 && tx <= NT - 2 && xf < nx;
-  if (PY) cell = cell && ty >= 1 && ty <= NTY - 2 && yf < ny;
-  const int64_t nm = MARCH ? p.n[MA] : 1;
-  const int64_t ra = MARCH ? (int64_t)chunk * p.H : 0;
-  const int64_t rb = MARCH ? min(ra + (int64_t)p.H, nm) : 1;
+  const int64_t yf = T::PY ? y0 - 1 + ty : 0;
+  bool cell = tx >= 1 && tx <= NT - 2 && xf < p.n[0];
+  if (T::PY) cell = cell && ty >= 1 && ty <= NTY - 2 && yf < p.n[1];
+  const int64_t ra = T::MARCH ? (int64_t)chunk * p.H : 0;
+  const int64_t rb = T::MARCH ? min(ra + (int64_t)p.H, p.n[T::MA]) : 1;
+  T t{p, st, p.us + p.origin + inst * p.si, p.un + p.origin + inst * p.si, p.out + p.origin + inst * p.si, smem,
+      p.kind == 0 ? 0.0 : *(volatile double*)&st->dt, tx, ty, x0, y0, xf, yf, cell, ra, rb, 0, 0u, {}};
+  t.co = t.pin(xf, yf);
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) t.smax[k] = 0.0;
 
-  // march-axis coordinate helper: face cell of this thread at march row r
-  auto OFF = [&](int64_t x, int64_t y, int64_t r) -> int64_t {
-    if constexpr (DIM == 1) return cell_off<1>(p, x, 0, 0);
-    else if constexpr (DIM == 2) return cell_off<2>(p, x, r, 0);
-    else return cell_off<3>(p, x, y, r);
-  };
-
-  unsigned errb = 0;  // bit a: degenerate HLLC fan on axis a
-  double smax[DIM];
+  double H[NC], G[NC], R[NC];
 #pragma unroll
-  for (int k = 0; k < DIM; ++k) smax[k] = 0.0;
-
-  // register window of this thread's column: A = u[r-1], B = u[r], C = u[r+1]
-  double A[NC], B[NC], C[NC];
-  double hiP[NC], GP[NC], resP[NC], unP[NC];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) { A[c] = B[c] = C[c] = hiP[c] = GP[c] = resP[c] = unP[c] = 0.0; }
-
-  int64_t rstart = MARCH ? ra - 1 : 0;
-  if constexpr (MARCH) {
-    load_nc<NC>(us, OFF(xf, yf, ra - 2), p.sc, A);
-    load_nc<NC>(us, OFF(xf, yf, ra - 1), p.sc, B);
-    load_nc<NC>(us, OFF(xf, yf, ra), p.sc, C);
-  } else {
-    load_nc<NC>(us, OFF(xf, yf, 0), p.sc, B);
-  }
-
-  for (int64_t r = rstart; r <= (MARCH ? rb : 0); ++r) {
-    double NX[NC], UNX[NC];
-    if constexpr (MARCH) {
-      if (r + 2 <= rb + 1) load_nc<NC>(us, OFF(xf, yf, r + 2), p.sc, NX);
-      if (p.kind >= 2 && cell && r >= ra && r < rb) {
-        const int64_t o = OFF(xf, yf, r);
-#pragma unroll
-        for (int c = 0; c < NC; ++c) UNX[c] = un[o + c * p.sc];
-      }
-      // ---- march axis: faces of row r, flux (r-1 | r), finish row r-1 ----
-      if (cell) {
-        double hiC[NC], loC[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) weno_faces<RECON>(A[c], B[c], C[c], p.P.eps, hiC[c], loC[c]);
-        if (r >= ra) {
-          double uL[NC], uR[NC], G[NC];
-#pragma unroll
-          for (int c = 0; c < NC; ++c) { uL[c] = hiP[c]; uR[c] = loC[c]; }
-          unsigned eb = 0;
-          interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, A, B, MA, p.P, G, eb);
-          if (eb) errb |= 1u << MA;
-          if (r - 1 >= ra) {
-            double v[NC];
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-#if FVB_FAST
-              const double Lc = fma(GP[c] - G[c], p.id[MA], resP[c]);
-#else
-              const double Lc = resP[c] - ddiv(G[c] - GP[c], p, MA);
-#endif
-              v[c] = rk_combine(p.kind, unP[c], A[c], dt, Lc);
-            }
-            const int64_t o = OFF(xf, yf, r - 1);
-#pragma unroll
-            for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
-            if (p.final_stage) post_cell<EQ, DIM, NC>(p, st, v, xf, yf, r - 1, smax);
-          }
-#pragma unroll
-          for (int c = 0; c < NC; ++c) GP[c] = G[c];
-        }
-#pragma unroll
-        for (int c = 0; c < NC; ++c) hiP[c] = hiC[c];
-      }
+  for (int c = 0; c < NC; ++c) H[c] = G[c] = R[c] = 0.0;
+  if constexpr (T::MARCH) {
+    double W0[NC], W1[NC], W2[NC];
+    t.load_col(ra - 2, W0);
+    t.load_col(ra - 1, W1);
+    t.load_col(ra, W2);
+#if FVB_TILE_UNROLL == 3
+    for (int64_t r = ra - 1; r <= rb; r += 3) {
+      t.row(r, W0, W1, W2, H, G, R);
+      if (r + 1 > rb) break;
+      t.row(r + 1, W1, W2, W0, H, G, R);
+      if (r + 2 > rb) break;
+      t.row(r + 2, W2, W0, W1, H, G, R);
     }
-
-    // ---- in-plane axes for row r ----
-    if (r >= ra && r < rb) {
-      // stage-start interior check (solver.py:90-93)
-      if constexpr (EQ == EQ_EULER) {
-        if (cell && !euler_physical<DIM>(B, p.P)) {
-          const long long key = ((long long)p.stage_idx << 42) | flat_cell<DIM>(p, xf, yf, MARCH ? r : 0);
-          atomicMin(&st->stage_err, key);
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < NC; ++c) sU(c, ty + OY, tx + 1) = B[c];
-      if constexpr (WENO) {
-        if ((!PY || (ty >= 1 && ty <= NTY - 2)) && (tx == 0 || tx == NT - 1)) {
-          const int64_t hxo = OFF(tx == 0 ? x0 - 2 : x0 + NT - 1, yf, r);
-          const int col = tx == 0 ? 0 : NT + 1;
-#pragma unroll
-          for (int c = 0; c < NC; ++c) sU(c, ty + OY, col) = __ldg(us + hxo + c * p.sc);
-        }
-        if constexpr (PY) {
-          if ((ty == 0 || ty == NTY - 1) && tx >= 1 && tx <= NT - 2) {
-            const int64_t hyo = OFF(xf, ty == 0 ? y0 - 2 : y0 + NTY - 1, r);
-            const int row = ty == 0 ? 0 : NTY + 1;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) sU(c, row, tx + 1) = __ldg(us + hyo + c * p.sc);
-          }
-        }
-      }
-      __syncthreads();
-      if constexpr (WENO) {
-        if (!PY || (ty >= 1 && ty <= NTY - 2)) {
-#pragma unroll
-          for (int c = 0; c < NC; ++c)
-            weno_faces<RECON>(sU(c, ty + OY, tx), sU(c, ty + OY, tx + 1), sU(c, ty + OY, tx + 2), p.P.eps,
-                              sHx(c, ty, tx), sLx(c, ty, tx));
-        }
-        if constexpr (PY) {
-          if (tx >= 1 && tx <= NT - 2) {
-#pragma unroll
-            for (int c = 0; c < NC; ++c)
-              weno_faces<RECON>(sU(c, ty, tx + 1), sU(c, ty + 1, tx + 1), sU(c, ty + 2, tx + 1), p.P.eps,
-                                sHy(c, ty, tx), sLy(c, ty, tx));
-          }
-        }
-        __syncthreads();
-      }
-      // interface fluxes: x interface tx sits between face cells tx-1 and tx
-      if (tx >= 1 && (!PY || (ty >= 1 && ty <= NTY - 2))) {
-        double uL[NC], uR[NC], cl[NC], cr[NC], G[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          cl[c] = sU(c, ty + OY, tx);
-          cr[c] = sU(c, ty + OY, tx + 1);
-          if constexpr (WENO) {
-            uL[c] = sHx(c, ty, tx - 1);
-            uR[c] = sLx(c, ty, tx);
-          } else {
-            uL[c] = cl[c];
-            uR[c] = cr[c];
-          }
-        }
-        unsigned eb = 0;
-        interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 0, p.P, G, eb);
-        if (eb && xf <= nx && (!PY || yf < ny)) errb |= 1u;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) sGx(c, ty, tx) = G[c];
-      }
-      if constexpr (PY) {
-        if (ty >= 1 && tx >= 1 && tx <= NT - 2) {
-          double uL[NC], uR[NC], cl[NC], cr[NC], G[NC];
-#pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            cl[c] = sU(c, ty, tx + 1);
-            cr[c] = sU(c, ty + 1, tx + 1);
-            if constexpr (WENO) {
-              uL[c] = sHy(c, ty - 1, tx);
-              uR[c] = sLy(c, ty, tx);
-            } else {
-              uL[c] = cl[c];
-              uR[c] = cr[c];
-            }
-          }
-          unsigned eb = 0;
-          interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 1, p.P, G, eb);
-          if (eb && yf <= ny && xf < nx) errb |= 2u;
-#pragma unroll
-          for (int c = 0; c < NC; ++c) sGy(c, ty, tx) = G[c];
-        }
-      }
-      __syncthreads();
-      if (cell) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-#if FVB_FAST
-          double res = (sGx(c, ty, tx) - sGx(c, ty, tx + 1)) * p.id[0];
-          if constexpr (PY) res = fma(sGy(c, ty, tx) - sGy(c, ty + 1, tx), p.id[1], res);
 #else
-          double res = 0.0 - ddiv(sGx(c, ty, tx + 1) - sGx(c, ty, tx), p, 0);
-          if constexpr (PY) res = res - ddiv(sGy(c, ty + 1, tx) - sGy(c, ty, tx), p, 1);
-#endif
-          resP[c] = res;
-        }
-        if constexpr (!MARCH) {
-          // 1D: the in-plane residual is the whole residual
-          double v[NC];
-          const int64_t o = OFF(xf, 0, 0);
-#pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            const double unc = p.kind >= 2 ? un[o + c * p.sc] : 0.0;
-            v[c] = rk_combine(p.kind, unc, B[c], dt, resP[c]);
-          }
-#pragma unroll
-          for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
-          if (p.final_stage) post_cell<EQ, DIM, NC>(p, st, v, xf, 0, 0, smax);
-        }
-      }
-    }
-    if constexpr (MARCH) {
+    // one copy of the row body (instruction-cache friendly); the window is
+    // rotated with register moves
+    for (int64_t r = ra - 1; r <= rb; ++r) {
+      t.row(r, W0, W1, W2, H, G, R);
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
-        A[c] = B[c];
-        B[c] = C[c];
-        C[c] = NX[c];
-        unP[c] = UNX[c];
+        const double w = W0[c];
+        W0[c] = W1[c];
+        W1[c] = W2[c];
+        W2[c] = w;
       }
     }
+#endif
+  } else {
+    double B[NC], unc[NC];
+    t.load_col(0, B);
+    t.inplane(0, B, R);
+    if (cell) {
+      if (p.kind >= 2) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) unc[c] = t.un[t.co + c * p.sc];
+      }
+      t.finish(0, B, unc, R);
+    }
   }
-
-  if (errb) {
+  if (t.errb) {
 #pragma unroll
     for (int a = 0; a < DIM; ++a)
-      if (errb & (1u << a))
+      if (t.errb & (1u << a))
         atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | ((long long)(1 + a) << 40));
   }
-  if (p.final_stage) block_epilogue<DIM>(p, st, inst, smax, true);
-#undef sU
-#undef sHx
-#undef sLx
-#undef sGx
-#undef sHy
-#undef sLy
-#undef sGy
+  if (p.final_stage) block_epilogue<DIM>(p, st, inst, t.smax, true);
 }
 
 template <int DIM, int EQ, int RECON, int NT, int NTY>
