@@ -160,6 +160,7 @@ static StageParams base_params(const fvb_scheme& s, const fvb_layout& L) {
   p.P.gm1 = s.gamma - 1.0;
   p.P.eps = s.weno_eps;
   for (int k = 0; k < 3; ++k) p.P.adv[k] = s.adv[k];
+  p.check_input = 1;
   p.ctl.dim = s.dim;
   p.ctl.cfl = s.cfl;
   p.ctl.t_end = s.t_end;
@@ -553,6 +554,9 @@ int fvb_run_begin(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, doub
   P.grid = stage_grid(*s, base, ninst);
   if (P.topo) base.nblocks *= (unsigned)ninst;  // one shared state counts every subdomain's blocks
   P.nstages = build_step(*s, *lay, P.bufs, base, P.stage);
+  // stage 1 reads u^n, already checked by the initial pass / the previous
+  // step's post-step check (physical, or wave_speed_maxima in run_parallel)
+  P.stage[0].check_input = 0;
   P.active = 1;
   // initial wave-speed pass + first dt (solver.py:211-224)
   StageParams sp = base;

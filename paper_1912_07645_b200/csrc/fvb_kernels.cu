@@ -22,24 +22,31 @@ void stage_block(int dim, int variant, int& nt, int& nty) {
   else { nt = Blk<3>::NT; nty = Blk<3>::NTY; }
 }
 
-template <int DIM, int EQ, int FLUX, int RECON>
-static int launch_one(const StageParams& p, dim3 grid, cudaStream_t s) {
+template <int DIM, int EQ, int FLUX, int RECON, bool FIN>
+static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
   if (DIM <= 2 && p.variant == 0) {
-    strip_kernel<DIM, EQ, FLUX, RECON, kStripWarps><<<grid, 32 * kStripWarps, 0, s>>>(p);
+    strip_kernel<DIM, EQ, FLUX, RECON, kStripWarps, FIN><<<grid, 32 * kStripWarps, 0, s>>>(p);
     return 0;
   } else {
-  constexpr int NT = Blk<DIM>::NT, NTY = Blk<DIM>::NTY;
-  constexpr int smem = stage_smem_bytes<DIM, EQ, RECON, NT, NTY>();
-  auto kern = stage_kernel<DIM, EQ, FLUX, RECON, NT, NTY>;
-  static bool attr_done = false;  // per instantiation
-  if (!attr_done) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_done = true;
+    constexpr int NT = Blk<DIM>::NT, NTY = Blk<DIM>::NTY;
+    constexpr int smem = stage_smem_bytes<DIM, EQ, RECON, NT, NTY>();
+    auto kern = stage_kernel<DIM, EQ, FLUX, RECON, NT, NTY, FIN>;
+    static bool attr_done = false;  // per instantiation
+    if (!attr_done) {
+      if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr_done = true;
+    }
+    kern<<<grid, dim3(NT, NTY), smem, s>>>(p);
+    return 0;
   }
-  kern<<<grid, dim3(NT, NTY), smem, s>>>(p);
-  return 0;
-  }
+}
+
+// the last stage of a step (post-step checks, CFL maxima, finalisation) is
+// a separate instantiation so the other stages carry none of its registers
+template <int DIM, int EQ, int FLUX, int RECON>
+static int launch_one(const StageParams& p, dim3 grid, cudaStream_t s) {
+  return p.final_stage ? launch_fin<DIM, EQ, FLUX, RECON, true>(p, grid, s)
+                       : launch_fin<DIM, EQ, FLUX, RECON, false>(p, grid, s);
 }
 
 template <int DIM>

@@ -24,9 +24,16 @@
 
 namespace fvb {
 
-// numpy.maximum / numpy.minimum: NaN-propagating (numerics.py:138,164-165)
+// numpy.maximum / numpy.minimum: NaN-propagating (numerics.py:138,164-165).
+// The fast mode uses the single-instruction fmax/fmin: they differ only on
+// NaN inputs, i.e. on states whose run is already failing a check.
+#if FVB_FAST
+__device__ __forceinline__ double np_max(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ double np_min(double a, double b) { return fmin(a, b); }
+#else
 __device__ __forceinline__ double np_max(double a, double b) { return (a > b || a != a) ? a : b; }
 __device__ __forceinline__ double np_min(double a, double b) { return (a < b || a != a) ? a : b; }
+#endif
 
 #if FVB_FAST
 // 1/x: MUFU seed + two Newton steps (full double precision for normal x)
@@ -178,6 +185,30 @@ __device__ __forceinline__ void weno_faces(double um, double uc, double up, doub
       lo = uc - 0.5 * (v0 * D1 + v1 * D0);
     }
 #endif
+  }
+}
+
+// All components of one cell: a warp whose every cell has a flat stencil
+// (um == uc == up, the uniform KH bands) skips the weights.  The shortcut
+// returns exactly what the formula gives for D0 = D1 = +0 (h = +0, so
+// hi = uc + 0.0 and lo = uc - 0.0, signed zeros included) in both modes.
+template <int NC, int RECON>
+__device__ __forceinline__ void weno_faces_nc(const double* um, const double* uc, const double* up, double eps,
+                                              double* hi, double* lo) {
+  if constexpr (RECON == RECON_NONE) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) { hi[c] = uc[c]; lo[c] = uc[c]; }
+  } else {
+    bool flat = true;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) flat &= (uc[c] == um[c]) & (up[c] == uc[c]);
+    if (!__any_sync(__activemask(), !flat)) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) { hi[c] = uc[c] + 0.0; lo[c] = uc[c] - 0.0; }
+      return;
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) weno_faces<RECON>(um[c], uc[c], up[c], eps, hi[c], lo[c]);
   }
 }
 

@@ -150,7 +150,7 @@ __device__ __forceinline__ void block_epilogue(const StageParams& p, FvbState* s
 // arrays rotated by NAME (no register moves) and the row after next loaded
 // into the slot that just died.
 // ---------------------------------------------------------------------------
-template <int DIM, int EQ, int FLUX, int RECON, int NT, int NTY>
+template <int DIM, int EQ, int FLUX, int RECON, int NT, int NTY, bool FIN>
 struct TileCtx {
   static constexpr int NC = NComp<EQ, DIM>::value;
   static constexpr bool WENO = RECON != RECON_NONE;
@@ -214,13 +214,13 @@ struct TileCtx {
     const int64_t o = co + roff(r);
 #pragma unroll
     for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
-    if (p.final_stage) post_cell<EQ, DIM, NC>(p, st, v, xf, PY ? yf : (MARCH ? r : 0), PY ? r : 0, smax);
+    if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v, xf, PY ? yf : (MARCH ? r : 0), PY ? r : 0, smax);
   }
 
   // in-plane axes (x; x and y in 3D) of row r: R <- residual of this cell
   __device__ __forceinline__ void inplane(int64_t r, const double* B, double* R) {
     if constexpr (EQ == EQ_EULER) {  // stage-start interior check (solver.py:90-93)
-      if (cell && !euler_physical<DIM>(B, p.P)) {
+      if (p.check_input && cell && !euler_physical<DIM>(B, p.P)) {
         const long long key = ((long long)p.stage_idx << 42) |
                               flat_cell<DIM>(p, xf, PY ? yf : (MARCH ? r : 0), PY ? r : 0);
         atomicMin(&st->stage_err, key);
@@ -247,17 +247,29 @@ struct TileCtx {
     __syncthreads();
     if constexpr (WENO) {
       if (!PY || (ty >= 1 && ty <= NTY - 2)) {
+        double um[NC], uc[NC], up[NC], hi[NC], lo[NC];
 #pragma unroll
-        for (int c = 0; c < NC; ++c)
-          weno_faces<RECON>(U(c, ty + OY, tx), U(c, ty + OY, tx + 1), U(c, ty + OY, tx + 2), p.P.eps,
-                            HX(c, ty, tx), LX(c, ty, tx));
+        for (int c = 0; c < NC; ++c) {
+          um[c] = U(c, ty + OY, tx);
+          uc[c] = U(c, ty + OY, tx + 1);
+          up[c] = U(c, ty + OY, tx + 2);
+        }
+        weno_faces_nc<NC, RECON>(um, uc, up, p.P.eps, hi, lo);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) { HX(c, ty, tx) = hi[c]; LX(c, ty, tx) = lo[c]; }
       }
       if constexpr (PY) {
         if (tx >= 1 && tx <= NT - 2) {
+          double um[NC], uc[NC], up[NC], hi[NC], lo[NC];
 #pragma unroll
-          for (int c = 0; c < NC; ++c)
-            weno_faces<RECON>(U(c, ty, tx + 1), U(c, ty + 1, tx + 1), U(c, ty + 2, tx + 1), p.P.eps,
-                              HY(c, ty, tx), LY(c, ty, tx));
+          for (int c = 0; c < NC; ++c) {
+            um[c] = U(c, ty, tx + 1);
+            uc[c] = U(c, ty + 1, tx + 1);
+            up[c] = U(c, ty + 2, tx + 1);
+          }
+          weno_faces_nc<NC, RECON>(um, uc, up, p.P.eps, hi, lo);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) { HY(c, ty, tx) = hi[c]; LY(c, ty, tx) = lo[c]; }
         }
       }
       __syncthreads();
@@ -335,8 +347,7 @@ struct TileCtx {
     }
     if (cell) {
       double hi[NC], lo[NC];
-#pragma unroll
-      for (int c = 0; c < NC; ++c) weno_faces<RECON>(A[c], B[c], C[c], p.P.eps, hi[c], lo[c]);
+      weno_faces_nc<NC, RECON>(A, B, C, p.P.eps, hi, lo);
       if (r >= ra) {
         double GC[NC];
         unsigned eb = 0;
@@ -371,10 +382,10 @@ struct TileCtx {
 #ifndef FVB_TILE_UNROLL
 #define FVB_TILE_UNROLL 1
 #endif
-template <int DIM, int EQ, int FLUX, int RECON, int NT, int NTY>
+template <int DIM, int EQ, int FLUX, int RECON, int NT, int NTY, bool FIN>
 __global__ void __launch_bounds__(NT * NTY, (DIM == 2 ? FVB_TILE_MINB : 1))
 stage_kernel(const StageParams p) {
-  using T = TileCtx<DIM, EQ, FLUX, RECON, NT, NTY>;
+  using T = TileCtx<DIM, EQ, FLUX, RECON, NT, NTY, FIN>;
   constexpr int NC = T::NC;
   extern __shared__ double smem[];
   int inst, chunk;
@@ -455,7 +466,7 @@ stage_kernel(const StageParams p) {
       if (t.errb & (1u << a))
         atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | ((long long)(1 + a) << 40));
   }
-  if (p.final_stage) block_epilogue<DIM>(p, st, inst, t.smax, true);
+  if constexpr (FIN) block_epilogue<DIM>(p, st, inst, t.smax, true);
 }
 
 template <int DIM, int EQ, int RECON, int NT, int NTY>
@@ -494,7 +505,7 @@ __device__ __forceinline__ void shfl_down_nc(const double* v, double* out) {
   for (int c = 0; c < NC; ++c) out[c] = __shfl_down_sync(0xffffffffu, v[c], 1);
 }
 
-template <int DIM, int EQ, int FLUX, int RECON>
+template <int DIM, int EQ, int FLUX, int RECON, bool FIN>
 struct StripCtx {
   static constexpr int NC = NComp<EQ, DIM>::value;
   const StageParams& p;
@@ -570,7 +581,7 @@ struct StripCtx {
     const int64_t o = xo + roff(r);
 #pragma unroll
     for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
-    if (p.final_stage) post_cell<EQ, DIM, NC>(p, st, v, xf, DIM == 2 ? r : 0, 0, smax);
+    if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v, xf, DIM == 2 ? r : 0, 0, smax);
   }
 
   __device__ __forceinline__ void stage_check(int64_t r, const double* uc) {
@@ -634,10 +645,10 @@ struct StripCtx {
   }
 };
 
-template <int DIM, int EQ, int FLUX, int RECON, int WPB>
+template <int DIM, int EQ, int FLUX, int RECON, int WPB, bool FIN>
 __global__ void __launch_bounds__(32 * WPB, FVB_STRIP_MINB)
 strip_kernel(const StageParams p) {
-  using S = StripCtx<DIM, EQ, FLUX, RECON>;
+  using S = StripCtx<DIM, EQ, FLUX, RECON, FIN>;
   constexpr int NC = S::NC;
   const int lane = threadIdx.x & 31;
   const int64_t strip = (int64_t)blockIdx.x * WPB + (threadIdx.x >> 5);
@@ -693,7 +704,7 @@ strip_kernel(const StageParams p) {
           atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | ((long long)(1 + a) << 40));
     }
   }
-  if (p.final_stage) block_epilogue<DIM>(p, st, inst, s.smax, true);
+  if constexpr (FIN) block_epilogue<DIM>(p, st, inst, s.smax, true);
 }
 
 // Standalone wave-speed pass: solver.py:128-136 (+ the initial is_physical

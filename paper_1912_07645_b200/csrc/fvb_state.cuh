@@ -153,6 +153,8 @@ struct StageParams {
   Phys P;
   int kind;           // 0: L  1: us+dt*L  2: RK2 final  3: RK3 stage 2  4: RK3 final
   int final_stage;    // 1: post-step checks + wave-speed maxima + finalize
+  int check_input;    // 1: stage-start physical check of u^(s) (solver.py:90-93); 0 when the
+                      //    previous step's post-check already covered it (stage 1 of a run)
   int stage_idx;      // stage number within the step (error ordering)
   int chunks;         // chunks along the march axis
   int H;              // rows per chunk
