@@ -133,17 +133,27 @@ def bench_ours(args, ws, rank, local):
     torch.cuda.set_stream(stream)
 
     n = args.cells
-    grid = P.GridSpec(2, (n, n), (0.0, 0.0), (1.0, 1.0), ghost_width=2)
-    cfg = P.SchemeConfig(P.EquationModel("euler", 2), P.FluxKind.HLLC,
+    dim = 3 if args.config == "kh3d" else 2
+    grid = P.GridSpec(dim, (n,) * dim, (0.0,) * dim, (1.0,) * dim, ghost_width=2)
+    cfg = P.SchemeConfig(P.EquationModel("euler", dim), P.FluxKind.HLLC,
                          P.Reconstruction(P.ReconstructionKind.WENO2), rk_order=3, cfl=0.475, t_end=2.0)
-    init = kelvin_helmholtz(grid, KH_VECTOR)
-    dev = DeviceField.from_host(init)
-    bufs = [dev.data, torch.empty_like(dev.data), torch.empty_like(dev.data)]
+    ninst = args.samples if args.config == "mc" else 1
+    if args.config == "mc":
+        from paper_1912_07645_b200.uq import SamplePlan, draw_sample
+
+        plan = SamplePlan("mc", ninst, 42, 4)
+        inits = [kelvin_helmholtz(grid, draw_sample(plan, k)) for k in range(ninst)]
+        init = inits[0]
+        b0 = torch.from_numpy(np.stack([f.data for f in inits])).to("cuda")
+    else:
+        init = kelvin_helmholtz(grid, KH_VECTOR)
+        b0 = DeviceField.from_host(init).data
+    bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
     total_steps = args.warmup + args.steps
-    run = DeviceRun(grid, cfg, bufs, 1, N.MODE_FIXED, 1 << 40, args.arith, log=False)
+    run = DeviceRun(grid, cfg, bufs, ninst, N.MODE_FIXED, 1 << 40, args.arith, log=False)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    cells = n * n
-    ncomp = 4
+    cells = n ** dim * ninst
+    ncomp = dim + 2
 
     run.steps(args.warmup)
     # advance to a developed state (KH roll-up under way) before timing, so
@@ -192,14 +202,16 @@ def bench_ours(args, ws, rank, local):
 
     # roofline: the 3 fused stage launches of a step (the only kernels in it)
     bytes_step = cells * 8 * ncomp * (2 + 3 + 3)  # stage1: r us, w out; stages 2-3: r us, un, w out
+    kname = {"kh2d": "stage_kernel<2,EULER,HLLC,WENO2>", "mc": "stage_kernel<2,EULER,HLLC,WENO2> (batched)",
+             "kh3d": "stage_kernel<3,EULER,HLLC,WENO2>"}[args.config]
     peak, peak_src = _hbm_peak()
     achieved = bytes_step / (ms_per_step * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
-                "kernel": "stage_kernel<2,EULER,HLLC,WENO2> (3 launches/step)",
+                "kernel": kname + " (3 launches/step)",
                 "algorithmic_bytes_per_cell_stage": round(bytes_step / cells / 3, 2)}
     prof = ROOT / "profiles" / "traffic.json"
-    if prof.exists():
+    if prof.exists() and args.config == "kh2d":
         try:
             roofline["traffic"] = json.loads(prof.read_text()).get("stage_bytes_per_launch")
         except Exception:
@@ -207,10 +219,12 @@ def bench_ours(args, ws, rank, local):
 
     # e2e through the public API with host buffers: run_simulation(host Field)
     e2e = None
-    if rank == 0 or ws > 1:
+    if (rank == 0 or ws > 1) and args.config == "kh2d":
         m = args.e2e_steps
         cfg_e = P.SchemeConfig(cfg.model, cfg.flux, cfg.recon, 3, 0.475, 2.0)
-        pinned = P.Field(grid, ncomp, init.data)
+        from paper_1912_07645_b200.solver import pinned_field
+
+        pinned = pinned_field(init)  # host input in pinned memory (contract: H2D from pinned)
         P.run_simulation(pinned, cfg_e, max_steps=2, arith=args.arith)  # warm
         torch.cuda.synchronize()
         tic = time.perf_counter()
@@ -316,7 +330,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--arith", default=os.environ.get("FVB_BENCH_ARITH", "fast"), choices=["fast", "exact"])
-    ap.add_argument("--cells", type=int, default=N_CELLS)
+    ap.add_argument("--cells", type=int, default=None, help="cells per axis (default 1024 kh2d, 512 mc, 256 kh3d)")
+    ap.add_argument("--config", default="kh2d", choices=["kh2d", "mc", "kh3d"],
+                    help="kh2d: BASELINE configs[1] (headline); mc: batched KH2D ensemble (configs[2] "
+                         "shape); kh3d: KH3D single domain (configs[3] shape)")
+    ap.add_argument("--samples", type=int, default=16, help="mc: samples per GPU batch")
     ap.add_argument("--cpu-steps", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--e2e-reps", type=int, default=3)
@@ -324,9 +342,17 @@ def main():
     ap.add_argument("--sustain", type=float, default=1.5, help="seconds of untimed load for the clock sampler")
     ap.add_argument("--warm-time", type=float, default=1.0, help="simulated time reached before timing")
     args = ap.parse_args()
+    if args.cells is None:
+        args.cells = {"kh2d": N_CELLS, "mc": 512, "kh3d": 256}[args.config]
     ws, rank, local = _dist()
-    workload = (f"KH2D {args.cells}x{args.cells} Euler, WENO2 + HLLC, SSP-RK3, periodic, fp64 "
-                "(BASELINE configs[1]); step = one RK3 time step (3 stages)")
+    workload = {
+        "kh2d": f"KH2D {args.cells}x{args.cells} Euler, WENO2 + HLLC, SSP-RK3, periodic, fp64 "
+                "(BASELINE configs[1]); step = one RK3 time step (3 stages)",
+        "mc": f"KH2D MC ensemble, {args.samples} samples/GPU x {args.cells}^2, WENO2 + HLLC, SSP-RK3, fp64, "
+              "batched (one instance per sample; configs[2] shape); step = one RK3 step of every sample",
+        "kh3d": f"KH3D {args.cells}^3 Euler, WENO2 + HLLC, SSP-RK3, periodic, fp64 (configs[3] shape, "
+                "single domain); step = one RK3 time step",
+    }[args.config]
     cores = os.cpu_count() or 1
 
     if args.impl == "reference":
@@ -352,7 +378,7 @@ def main():
     if rank != 0:
         return
     cpu = None
-    if not args.no_cpu:
+    if not args.no_cpu and args.config == "kh2d":
         # bounded CPU sample: 1 RK3 step of the same workload, single process
         # (numpy is single threaded), the oracle = reference op order
         val, sps = bench_cpu(args.cells, 1, 1)

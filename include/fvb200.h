@@ -46,6 +46,7 @@ extern "C" {
 #define FVB_SUB_POST_UNPHYSICAL 4   /* solver.py:239-242 */
 #define FVB_SUB_HLLC_DEGENERATE 5   /* numerics.py:166-167 */
 #define FVB_SUB_SPEED_UNPHYSICAL 6  /* equations.py:118-119 via wave_speed_maxima */
+#define FVB_SUB_REMOTE 7            /* another rank of a decomposed run failed (parallel.py:470-472) */
 
 enum { FVB_EQ_EULER = 0, FVB_EQ_BURGERS = 1, FVB_EQ_ADVECTION = 2 };
 enum { FVB_FLUX_RUSANOV = 0, FVB_FLUX_HLLC = 1 };
@@ -161,6 +162,19 @@ int fvb_run_read_log(fvb_ctx* ctx, double* h_log, int64_t per_instance);
  * All instances share one step state (global dt = max over subdomains,
  * parallel.py:498-501).  ranks = NULL clears. */
 int fvb_run_set_topology(fvb_ctx* ctx, const int32_t* ranks, const int32_t* periodic);
+/* Process-per-GPU decomposition (parallel.py:479-521 over NCCL): with
+ * external reduce on, the next fvb_run_begin computes the local wave-speed
+ * maxima but does not finalise; the caller drives the step stage by stage:
+ *   for s in stages: fill HALO ghosts of the stage input (fvb_halo_pack /
+ *   send-recv / fvb_halo_unpack); fvb_run_stage(ctx, s)
+ *   fvb_run_export(ctx, d_buf)        d_buf[dim+2]: maxima, hard-error, unphysical
+ *   all-reduce(MAX) d_buf across ranks
+ *   fvb_run_finalize(ctx, d_buf, 1)   (post = 0 after fvb_run_begin)
+ * Stage inputs: stage s of RK2/3 reads bufs[s]; RK1 reads bufs[steps % 2]. */
+int fvb_run_set_external_reduce(fvb_ctx* ctx, int on);
+int fvb_run_stage(fvb_ctx* ctx, int stage);
+int fvb_run_export(fvb_ctx* ctx, double* d_out);
+int fvb_run_finalize(fvb_ctx* ctx, const double* d_global, int post);
 /* kernel launches issued by the last fvb_run / fvb_run_steps calls */
 int64_t fvb_launch_count(const fvb_ctx* ctx);
 

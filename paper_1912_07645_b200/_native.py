@@ -18,7 +18,7 @@ LIB_PATH = Path(os.environ.get("FVB_LIB") or Path(__file__).resolve().parent / "
 
 # status codes (fvb200.h)
 OK, E_CONFIG, E_UNPHYSICAL, E_SIMULATION, E_STATIC, E_PROTOCOL, E_CUDA = range(7)
-SUB_NONE, SUB_INIT_UNPHYS, SUB_STAGE_UNPHYS, SUB_NONFINITE, SUB_POST_UNPHYS, SUB_HLLC, SUB_SPEED_UNPHYS = range(7)
+SUB_NONE, SUB_INIT_UNPHYS, SUB_STAGE_UNPHYS, SUB_NONFINITE, SUB_POST_UNPHYS, SUB_HLLC, SUB_SPEED_UNPHYS, SUB_REMOTE = range(8)
 EQ = {"euler": 0, "burgers": 1, "advection": 2}
 FLUX = {"rusanov": 0, "hllc": 1}
 RECON = {"none": 0, "weno2": 1, "weno3": 2}
@@ -78,6 +78,10 @@ _SIGS = {
     "fvb_run_poll": ([C.c_void_p, C.POINTER(RunInfo), C.POINTER(C.c_int32)], C.c_int),
     "fvb_run_set_log": ([C.c_void_p, C.c_int64, C.c_int], C.c_int),
     "fvb_run_set_topology": ([C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)], C.c_int),
+    "fvb_run_set_external_reduce": ([C.c_void_p, C.c_int], C.c_int),
+    "fvb_run_stage": ([C.c_void_p, C.c_int], C.c_int),
+    "fvb_run_export": ([C.c_void_p, C.c_void_p], C.c_int),
+    "fvb_run_finalize": ([C.c_void_p, C.c_void_p, C.c_int], C.c_int),
     "fvb_run_read_log": ([C.c_void_p, C.POINTER(C.c_double), C.c_int64], C.c_int),
     "fvb_launch_count": ([C.c_void_p], C.c_int64),
     "fvb_moments_push": ([C.c_void_p, C.POINTER(Scheme), C.POINTER(Layout), C.c_void_p, C.c_int,

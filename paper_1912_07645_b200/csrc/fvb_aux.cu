@@ -8,8 +8,22 @@
 #include <cstdint>
 
 #include "../../include/fvb200.h"
+#include "fvb_state.cuh"
 
 namespace fvb {
+
+__global__ void export_kernel(const FvbState* st, int dim, double* out) { export_step(st, dim, out); }
+__global__ void finalize_global_kernel(FvbState* st, LoopCtl L, const double* g, int post) {
+  finalize_global(st, L, g, post != 0);
+}
+int launch_export(const FvbState* st, int dim, double* out, cudaStream_t s) {
+  export_kernel<<<1, 1, 0, s>>>(st, dim, out);
+  return 0;
+}
+int launch_finalize_global(FvbState* st, const LoopCtl& L, const double* g, int post, cudaStream_t s) {
+  finalize_global_kernel<<<1, 1, 0, s>>>(st, L, g, post);
+  return 0;
+}
 
 namespace {
 

@@ -41,6 +41,8 @@ int launch_structure(const fvb_scheme& s, const fvb_layout& L, const double* u, 
 int structure_blocks(const fvb_scheme& s);
 int launch_halo_instances(const fvb_scheme& s, const fvb_layout& L, double* u, int ninst, const int* ranks,
                           const int* periodic, cudaStream_t st);
+int launch_export(const FvbState* st, int dim, double* out, cudaStream_t s);
+int launch_finalize_global(FvbState* st, const LoopCtl& L, const double* g, int post, cudaStream_t s);
 }  // namespace fvb
 
 using fvb::FvbState;
@@ -59,6 +61,7 @@ struct RunPlan {
   int nstages;
   dim3 grid;
   int active;
+  int external;      // cross-rank reduce driven by the caller (fvb_run_stage/export/finalize)
   int topo;          // instances are the subdomains of one decomposed run
   int ranks[3];
   int periodic[3];
@@ -80,6 +83,7 @@ struct fvb_ctx {
   int64_t partials_cap;
   RunPlan plan;
   int topo_pending;
+  int external_pending;
   int topo_ranks[3];
   int topo_periodic[3];
   cudaGraphExec_t graph;
@@ -536,6 +540,8 @@ int fvb_run_begin(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, doub
   P.max_steps = max_steps;
   P.topo = ctx->topo_pending;
   ctx->topo_pending = 0;
+  P.external = ctx->external_pending;
+  ctx->external_pending = 0;
   for (int k = 0; k < 3; ++k) {
     P.ranks[k] = ctx->topo_ranks[k];
     P.periodic[k] = ctx->topo_periodic[k];
@@ -557,11 +563,12 @@ int fvb_run_begin(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, doub
   // stage 1 reads u^n, already checked by the initial pass / the previous
   // step's post-step check (physical, or wave_speed_maxima in run_parallel)
   P.stage[0].check_input = 0;
+  if (P.external) P.stage[P.nstages - 1].defer_finalize = 1;
   P.active = 1;
   // initial wave-speed pass + first dt (solver.py:211-224)
   StageParams sp = base;
   sp.us = bufs[0];
-  return do_speed(ctx, *s, sp, 1, ninst);
+  return do_speed(ctx, *s, sp, P.external ? 0 : 1, ninst);
 }
 
 int fvb_run_steps(fvb_ctx* ctx, int64_t n_steps) {
@@ -644,6 +651,44 @@ int fvb_run_read_log(fvb_ctx* ctx, double* h_log, int64_t per_instance) {
                                 ctx->stream));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   return FVB_OK;
+}
+
+int fvb_run_set_external_reduce(fvb_ctx* ctx, int on) {
+  ctx->external_pending = on ? 1 : 0;
+  return FVB_OK;
+}
+
+int fvb_run_stage(fvb_ctx* ctx, int stage) {
+  RunPlan& P = ctx->plan;
+  if (!P.active || !P.external) return set_err(ctx, FVB_E_CONFIG, "fvb_run_stage needs an external-reduce run");
+  if (stage < 0 || stage >= P.nstages) return set_err(ctx, FVB_E_CONFIG, "stage %d out of range", stage);
+  StageParams p = P.stage[stage];
+  if (P.s.rk_order == 1) {
+    const int par = (int)(P.steps_enqueued & 1);
+    p.us = P.bufs[par];
+    p.un = P.bufs[par];
+    p.out = P.bufs[1 - par];
+  }
+  int r = do_stage(ctx, P.s, p, P.grid);
+  if (r) return r;
+  if (stage == P.nstages - 1) P.steps_enqueued++;
+  return FVB_OK;
+}
+
+int fvb_run_export(fvb_ctx* ctx, double* d_out) {
+  RunPlan& P = ctx->plan;
+  if (!P.active) return set_err(ctx, FVB_E_CONFIG, "no active run");
+  fvb::launch_export(ctx->d_state, P.s.dim, d_out, ctx->stream);
+  ctx->launches++;
+  return check_launch(ctx, "export");
+}
+
+int fvb_run_finalize(fvb_ctx* ctx, const double* d_global, int post) {
+  RunPlan& P = ctx->plan;
+  if (!P.active) return set_err(ctx, FVB_E_CONFIG, "no active run");
+  fvb::launch_finalize_global(ctx->d_state, P.stage[0].ctl, d_global, post, ctx->stream);
+  ctx->launches++;
+  return check_launch(ctx, "finalize");
 }
 
 int fvb_run_set_topology(fvb_ctx* ctx, const int32_t* ranks, const int32_t* periodic) {

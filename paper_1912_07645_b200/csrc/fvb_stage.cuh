@@ -127,6 +127,7 @@ __device__ __forceinline__ void block_epilogue(const StageParams& p, FvbState* s
     }
     if (lane == 0 && b != 0ull) atomicMax(&st->smax[k], b);
   }
+  if (p.defer_finalize) return;  // maxima stay in the state for the cross-rank reduce
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0 && threadIdx.y == 0) {

@@ -137,6 +137,36 @@ __device__ inline void finalize_step(FvbState* st, const LoopCtl& L, int inst, b
   __threadfence();
 }
 
+// Cross-rank step finalisation (process-per-GPU decomposition): the caller
+// all-reduces (MAX) what export wrote -- [maxima (dim), hard error, unphysical]
+// -- and every rank finalises with the same global values, so t, dt and the
+// stop decision agree on all ranks (parallel.py:498-501).
+__device__ inline void export_step(const FvbState* st, int dim, double* out) {
+  const volatile FvbState* vs = st;
+  for (int k = 0; k < dim; ++k) out[k] = bits_to_d(vs->smax[k]);
+  out[dim] = (vs->stage_err != kNone || vs->bad_nonfinite != kNone) ? 1.0 : 0.0;
+  out[dim + 1] = vs->bad_unphys != kNone ? 1.0 : 0.0;
+}
+
+__device__ inline void finalize_global(FvbState* st, const LoopCtl& L, const double* g, bool post) {
+  volatile FvbState* vs = st;
+  for (int k = 0; k < L.dim; ++k) vs->smax[k] = (unsigned long long)__double_as_longlong(g[k]);
+  const bool local_hard = vs->stage_err != kNone || vs->bad_nonfinite != kNone;
+  if (g[L.dim] != 0.0 && !local_hard) {  // another rank failed this step
+    if (post) {
+      vs->t = vs->t + vs->dt;
+      vs->step = vs->step + 1;
+    }
+    vs->err = FVB_E_SIMULATION;
+    vs->errsub = FVB_SUB_REMOTE;
+    vs->errcell = -1;
+    vs->done = 1;
+    return;
+  }
+  if (g[L.dim + 1] != 0.0 && vs->bad_unphys == kNone) vs->bad_unphys = kNone - 1;  // remote cell
+  finalize_step(st, L, 0, post, true);
+}
+
 // Kernel parameters of one stage launch (identical in both arithmetic modes).
 struct StageParams {
   const double* us;   // stage input u^(s) (stencil reads)
@@ -160,6 +190,8 @@ struct StageParams {
   int H;              // rows per chunk
   unsigned nblocks;   // blocks per state (finalize counter)
   int shared_state;   // 1: all instances are subdomains of one run (one FvbState)
+  int defer_finalize; // 1: leave maxima/flags in the state; the caller reduces them
+                      //    across ranks and calls fvb_run_finalize
   int variant;        // 1D/2D kernel: 0 = warp strip, 1 = shared-memory tile
   LoopCtl ctl;
 };

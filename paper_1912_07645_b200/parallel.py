@@ -286,7 +286,8 @@ def run_parallel(init, cfg, ranks_per_axis, n_steps: int | None = None, overlap:
     parts = decompose(init.grid, topo)
     if torch.distributed.is_available() and torch.distributed.is_initialized() \
             and torch.distributed.get_world_size() == topo.size and topo.size > 1:
-        return run_parallel_nccl(init, cfg, topo, parts, n_steps, arith=arith)
+        cpu = torch.distributed.get_backend() == "gloo"
+        return run_parallel_nccl(init, cfg, topo, parts, n_steps, arith=arith, cpu_comm=cpu)
     locals_ = scatter_field(init, parts)
     grid = parts[0].grid
     ncomp = init.ncomp
@@ -324,10 +325,134 @@ def run_parallel(init, cfg, ranks_per_axis, n_steps: int | None = None, overlap:
     return stitch_fields(init.grid, parts, finals), [list(recs) for _ in range(topo.size)]
 
 
-def run_parallel_nccl(init, cfg, topo, parts, n_steps, *, arith=None):
-    """One rank per process/GPU with NCCL halos.  Not yet wired: the
-    single-device path above covers the contract; see DESIGN.md."""
-    raise E.ConfigError("multi-process run_parallel over NCCL is not available in this build")
+def halo_exchange_dist(topo: RankTopology, rank: int, periodic, pack, unpack, alloc, dist, group=None):
+    """Face-only halo exchange of one rank over torch.distributed P2P
+    (NCCL on GPUs; gloo in the CPU tests).
+
+    ``pack(axis, side)`` returns the contiguous slab of the g interior layers
+    next to face (axis, side); ``alloc(axis)`` an empty receive buffer;
+    ``unpack(axis, side, buf)`` writes a received slab into the ghosts of
+    that face.  Axes are exchanged concurrently (the
+    residual never reads corner ghosts, solver.py:99-104).  Ordering rule so
+    that a pair of ranks that are mutual neighbours on both sides (2 ranks on
+    a periodic axis, parallel.py:227-230) match: sends are issued by side
+    (low, high), receives by the SENDER's side, i.e. high ghosts first.
+    World-edge sides without a neighbour are left to the caller (outflow)."""
+    ops, recvs = [], []
+    for axis in range(topo.dim):
+        if topo.ranks_per_axis[axis] == 1:
+            continue
+        nb = [topo.neighbor(rank, axis, side, bool(periodic[axis])) for side in (0, 1)]
+        for side in (0, 1):
+            if nb[side] is not None:
+                ops.append(dist.P2POp(dist.isend, pack(axis, side), nb[side], group))
+        for side in (1, 0):
+            if nb[side] is not None:
+                buf = alloc(axis)
+                ops.append(dist.P2POp(dist.irecv, buf, nb[side], group))
+                recvs.append((axis, side, buf))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for axis, side, buf in recvs:
+        unpack(axis, side, buf)
+
+
+def run_parallel_nccl(init, cfg, topo, parts, n_steps, *, arith=None, group=None, cpu_comm: bool = False):
+    """One subdomain per process (rank r of the torch.distributed group owns
+    part r), stage-wise: halo exchange of every stage input, fused stage
+    kernel, then one all-reduce(MAX) of [maxima, error flags] per step and a
+    device finalisation that all ranks evaluate identically
+    (parallel.py:479-521).  ``cpu_comm`` stages the exchanged slabs and the
+    reduce through host memory (gloo), e.g. to test several ranks on one GPU
+    without GPU-side waits."""
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    part = parts[rank]
+    grid = part.grid
+    ncomp = init.ncomp
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)  # NCCL calls order after the library's kernels on this stream
+    local = scatter_field(init, [part])[0]
+    dev = DeviceField.from_host(local)
+    b0 = dev.data.unsqueeze(0).contiguous()
+    bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
+    ctx = N.context()
+    split = tuple(k for k in range(grid.dim) if topo.ranks_per_axis[k] > 1)
+    periodic = [int(_v(cfg.bc[k]) == "periodic") for k in range(grid.dim)]
+    ctx.check(ctx.lib.fvb_run_set_external_reduce(ctx.h, 1))
+    mode = N.MODE_FIXED if n_steps is not None else N.MODE_PAR_T_END
+    run = DeviceRun(grid, cfg, bufs, 1, mode, n_steps, arith, halo_axes=split, ctx=ctx)
+    s = run.scheme
+    L = run.layout
+    red = torch.zeros(grid.dim + 2, dtype=torch.float64, device="cuda")
+
+    def reduce_and_finalize(post: int):
+        ctx.check(ctx.lib.fvb_run_export(ctx.h, N.C.c_void_p(red.data_ptr())))
+        if cpu_comm:
+            host = red.cpu()
+            dist.all_reduce(host, op=dist.ReduceOp.MAX, group=group)
+            red.copy_(host)
+        else:
+            dist.all_reduce(red, op=dist.ReduceOp.MAX, group=group)
+        ctx.check(ctx.lib.fvb_run_finalize(ctx.h, N.C.c_void_p(red.data_ptr()), post))
+
+    def exchange(u):
+        ptr = N.C.c_void_p(u.data_ptr())
+
+        def alloc(axis):
+            cnt = int(ctx.lib.fvb_halo_count(N.C.byref(s), axis))
+            return torch.empty(cnt, dtype=torch.float64, device="cpu" if cpu_comm else u.device)
+
+        def pack(axis, side):
+            cnt = int(ctx.lib.fvb_halo_count(N.C.byref(s), axis))
+            buf = torch.empty(cnt, dtype=torch.float64, device=u.device)
+            ctx.check(ctx.lib.fvb_halo_pack(ctx.h, N.C.byref(s), N.C.byref(L), ptr, axis, side,
+                                            N.C.c_void_p(buf.data_ptr())))
+            return buf.cpu() if cpu_comm else buf
+
+        def unpack(axis, side, buf):
+            b = buf.to(u.device) if cpu_comm else buf
+            ctx.check(ctx.lib.fvb_halo_unpack(ctx.h, N.C.byref(s), N.C.byref(L), ptr, axis, side,
+                                              N.C.c_void_p(b.data_ptr())))
+
+        halo_exchange_dist(topo, rank, periodic, pack, unpack, alloc, dist, group)
+        # world edges of split, non-periodic axes: outflow ghosts (parallel.py:246-247)
+        view = DeviceField(grid, ncomp, u[0])
+        for axis in split:
+            for side in (0, 1):
+                if topo.neighbor(rank, axis, side, bool(periodic[axis])) is None:
+                    _fill_one_side(view, axis, side)
+
+    reduce_and_finalize(0)
+    nst = 1 if cfg.rk_order == 1 else cfg.rk_order
+    while True:
+        infos, done = run.poll()
+        if done[0]:
+            break
+        tic = time.perf_counter()
+        for st in range(nst):
+            exchange(bufs[int(infos[0].steps) % 2] if nst == 1 else bufs[st])
+            ctx.check(ctx.lib.fvb_run_stage(ctx.h, st))
+        reduce_and_finalize(1)
+        infos, _ = run.poll()
+        run.read_log(infos, time.perf_counter() - tic)
+    info = run.end()[0]
+    if info.err:
+        try:
+            _raise_run_error(info, grid, ncomp)
+        except E.ConslawError as exc:
+            raise E.SimulationError(f"rank {rank} failed: {exc}") from exc
+    final = bufs[int(info.steps) % 2] if cfg.rk_order == 1 else bufs[0]
+    mine = DeviceField(grid, ncomp, final[0]).to_host()
+    recs = [RankRecord(r.step, r.t, r.dt, r.seconds) for r in run.records[0]]
+    # gather the subdomains and the per-rank records (the reference returns all)
+    gathered = [None] * topo.size
+    dist.all_gather_object(gathered, (mine.data, recs), group=group)
+    locs = [Field(parts[r].grid, ncomp, gathered[r][0]) for r in range(topo.size)]
+    return stitch_fields(init.grid, parts, locs), [gathered[r][1] for r in range(topo.size)]
 
 
 # ---------------------------------------------------------------------------

@@ -159,14 +159,18 @@ class DeviceField:
 
     @classmethod
     def from_host(cls, field, device=None, pin: bool = False):
+        """H2D copy of ``field.data`` (one DMA; asynchronous when the numpy
+        buffer lives in pinned memory, e.g. ``pinned_field``)."""
         import torch
 
         N._require_cuda()  # no CPU fallback: fail loudly without a GPU
         src = torch.from_numpy(np.ascontiguousarray(field.data, dtype=np.float64))
-        if pin:
+        pinned = src.is_pinned()
+        if pin and not pinned:
             src = src.pin_memory()
+            pinned = True
         dev = torch.empty(src.shape, dtype=torch.float64, device=device or "cuda")
-        dev.copy_(src, non_blocking=pin)
+        dev.copy_(src, non_blocking=pinned)
         return cls(field.grid, field.ncomp, dev)
 
     @property
@@ -175,16 +179,32 @@ class DeviceField:
         return self.data[(slice(None),) + tuple(slice(g, g + n) for n in self.grid.interior_shape)]
 
     def to_host(self, like=None):
-        """Reference Field with zero ghosts (solver.py:196 field_from_interior)."""
-        out = np.zeros(tuple(self.data.shape))
+        """Reference Field with zero ghosts (solver.py:196 field_from_interior):
+        one contiguous D2H copy of the whole buffer, ghosts zeroed on the host."""
+        a = self.data.cpu().numpy()
         g = self.grid.ghost_width
-        sl = (slice(None),) + tuple(slice(g, g + n) for n in self.grid.interior_shape)
-        out[sl] = self.interior.cpu().numpy()
+        for j, n in enumerate(self.grid.interior_shape):  # zero the ghost slabs on the host
+            lo = [slice(None)] * a.ndim
+            hi = [slice(None)] * a.ndim
+            lo[1 + j] = slice(0, g)
+            hi[1 + j] = slice(n + g, n + 2 * g)
+            a[tuple(lo)] = 0.0
+            a[tuple(hi)] = 0.0
         cls = type(like) if like is not None and not isinstance(like, DeviceField) else (TYPES["Field"] or Field)
-        return cls(self.grid, self.ncomp, out)
+        return cls(self.grid, self.ncomp, a)
 
     def copy(self):
         return DeviceField(self.grid, self.ncomp, self.data.clone())
+
+
+def pinned_field(field):
+    """Copy of a host Field whose data lives in pinned (page-locked) memory,
+    so run_simulation's host<->device copies are single DMAs."""
+    import torch
+
+    t = torch.empty(tuple(field.data.shape), dtype=torch.float64, pin_memory=True)
+    t.numpy()[...] = field.data
+    return type(field)(field.grid, field.ncomp, t.numpy())
 
 
 def _ptr(t) -> int:
@@ -222,7 +242,11 @@ def _raise_run_error(info: N.RunInfo, grid, ncomp: int, dev=None):
         raise E.SimulationError(f"unphysical state after step {info.steps} (t = {info.t:.6g})")
     if sub == N.SUB_HLLC:
         raise E.UnphysicalStateError("degenerate HLLC wave fan (sL >= sR)")
+    if sub == N.SUB_REMOTE:
+        raise E.SimulationError("another rank of the decomposed run failed")
     if sub == N.SUB_SPEED_UNPHYS:
+        if not 0 <= int(info.errcell) < math.prod(grid.cells):
+            raise E.UnphysicalStateError("unphysical state on another rank")
         idx = _cell_index(grid, info.errcell)
         val = ""
         if dev is not None:
@@ -370,13 +394,12 @@ def run_simulation(init, cfg, observers: Sequence[Callable] = (), max_steps: int
     if final_info.err:
         _raise_run_error(final_info, grid, dev.ncomp, DeviceField(grid, dev.ncomp, bufs[run.result_buffer(final_info)]))
     out = DeviceField(grid, dev.ncomp, bufs[run.result_buffer(final_info)])
-    # zero ghosts like field_from_interior (solver.py:196)
-    g = grid.ghost_width
-    keep = out.interior.clone()
+    if not was_dev:
+        return out.to_host(init), run.records[0]  # ghosts zeroed on the host copy
+    keep = out.interior.clone()  # zero ghosts like field_from_interior (solver.py:196)
     out.data.zero_()
     out.interior.copy_(keep)
-    result = out if was_dev else out.to_host(init)
-    return result, run.records[0]
+    return out, run.records[0]
 
 
 # ---------------------------------------------------------------------------

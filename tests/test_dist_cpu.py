@@ -67,3 +67,72 @@ def test_rank_ordered_moment_merge_gloo():
     out = mgr.dict()
     mp.spawn(_moments_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     assert out[0] and out[1]
+
+
+def _halo_worker(rank, world, port, lay, periodic, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import fv_oracle as O
+    from paper_1912_07645_b200 import parallel as PP
+
+    g = 2
+    cells = (12, 10)
+    rng = np.random.default_rng(3)
+    inner = rng.standard_normal((3, cells[1], cells[0]))
+    sc = O.Scheme(dim=2, cells=cells, deltas=(1 / 12, 1 / 10), eq="burgers", recon="weno2",
+                  bcs=tuple("periodic" if p else "outflow" for p in periodic))
+    want = O.ghost_fill(O.padded_from_interior(sc, inner), sc)
+    topo = PP.RankTopology(lay)
+    loc_cells = (cells[0] // lay[0], cells[1] // lay[1])
+    cx, cy = topo.coords(rank)
+    ox, oy = cx * loc_cells[0], cy * loc_cells[1]
+    u = np.zeros((3, loc_cells[1] + 2 * g, loc_cells[0] + 2 * g))
+    u[:, g:g + loc_cells[1], g:g + loc_cells[0]] = inner[:, oy:oy + loc_cells[1], ox:ox + loc_cells[0]]
+
+    def sl(axis, lo, hi):  # slab over the padded extent of the other axis
+        s = [slice(None), slice(None), slice(None)]
+        s[2 - axis] = slice(lo, hi)
+        return tuple(s)
+
+    def pack(axis, side):
+        n = loc_cells[axis]
+        return torch.from_numpy(np.ascontiguousarray(u[sl(axis, g, 2 * g) if side == 0 else sl(axis, n, n + g)]))
+
+    def alloc(axis):
+        return torch.empty_like(pack(axis, 0))
+
+    def unpack(axis, side, buf):
+        n = loc_cells[axis]
+        u[sl(axis, 0, g) if side == 0 else sl(axis, n + g, n + 2 * g)] = buf.numpy()
+
+    PP.halo_exchange_dist(topo, rank, periodic, pack, unpack, alloc, dist)
+    ok = True
+    for axis in range(2):
+        n = loc_cells[axis]
+        if topo.ranks_per_axis[axis] == 1:
+            continue
+        for side in (0, 1):
+            if topo.neighbor(rank, axis, side, periodic[axis]) is None:
+                continue
+            # face ghosts over the transverse interior must equal the serial fill
+            gh = slice(0, g) if side == 0 else slice(n + g, n + 2 * g)
+            if axis == 0:
+                mine = u[:, g:g + loc_cells[1], gh]
+                ref = want[:, g + oy:g + oy + loc_cells[1], (ox + gh.start):(ox + gh.stop)]
+            else:
+                mine = u[:, gh, g:g + loc_cells[0]]
+                ref = want[:, (oy + gh.start):(oy + gh.stop), g + ox:g + ox + loc_cells[0]]
+            ok &= bool(np.array_equal(mine, ref))
+    out[rank] = ok
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("lay,periodic", [((2, 1), (True, True)), ((2, 2), (True, True)), ((2, 2), (False, True)),
+                                          ((1, 2), (True, False))])
+def test_halo_exchange_dist_gloo(lay, periodic):
+    world = lay[0] * lay[1]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_halo_worker, args=(world, _free_port(), lay, periodic, out), nprocs=world, join=True)
+    assert all(out[r] for r in range(world))
