@@ -176,9 +176,12 @@ static StageParams base_params(const fvb_scheme& s, const fvb_layout& L) {
 static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst) {
   int nt, nty;
   const char* kv = getenv("FVB_KERNEL");
-  // 2D default: shared-memory tile kernel (fastest measured);
-  // FVB_KERNEL=strip selects the warp-strip kernel
-  p.variant = (kv && std::strcmp(kv, "strip") == 0) ? 0 : 1;
+  // 2D default: the cp.async ring kernel (fastest measured);
+  // FVB_KERNEL=tile / strip select the register-window variants
+  p.variant = 2;
+  if (kv && std::strcmp(kv, "strip") == 0) p.variant = 0;
+  if (kv && std::strcmp(kv, "tile") == 0) p.variant = 1;
+  if (s.dim != 2 && p.variant == 2) p.variant = 1;
   if (s.arith == FVB_ARITH_FAST) fvb::fast::stage_block(s.dim, p.variant, nt, nty);
   else fvb::exact::stage_block(s.dim, p.variant, nt, nty);
   const int64_t strips = (p.n[0] + (nt - 2) - 1) / (nt - 2);

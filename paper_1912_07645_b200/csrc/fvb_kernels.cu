@@ -16,6 +16,7 @@ constexpr int kStripWarps = 4;
 
 // cells per block along x (reported as nt-2) and the y tile (nty-2, 3D only)
 void stage_block(int dim, int variant, int& nt, int& nty) {
+  if (dim == 1 && variant == 2) variant = 1;
   if (dim <= 2 && variant == 0) { nt = kStripCells * kStripWarps + 2; nty = 1; }
   else if (dim == 1) { nt = Blk<1>::NT; nty = 1; }
   else if (dim == 2) { nt = Blk<2>::NT; nty = 1; }
@@ -24,6 +25,14 @@ void stage_block(int dim, int variant, int& nt, int& nty) {
 
 template <int DIM, int EQ, int FLUX, int RECON, bool FIN>
 static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
+  if constexpr (DIM == 2) {
+    if (p.variant == 2) {
+      constexpr int NT = Blk<2>::NT;
+      constexpr int smem = ring_smem_bytes<EQ, RECON, NT>();
+      ring_kernel<EQ, FLUX, RECON, NT, FIN><<<grid, NT, smem, s>>>(p);
+      return 0;
+    }
+  }
   if (DIM <= 2 && p.variant == 0) {
     strip_kernel<DIM, EQ, FLUX, RECON, kStripWarps, FIN><<<grid, 32 * kStripWarps, 0, s>>>(p);
     return 0;

@@ -708,6 +708,223 @@ strip_kernel(const StageParams p) {
   if constexpr (FIN) block_epilogue<DIM>(p, st, inst, s.smax, true);
 }
 
+// ---------------------------------------------------------------------------
+// 2D ring kernel (variant 2): the tile kernel with the march window moved
+// out of registers into a shared-memory ring of rows filled by cp.async
+// (LDGSTS) PD rows ahead.  Loads never stall the math (no long-scoreboard
+// waits, no register moves of freshly loaded data), the x phase reads its
+// row straight from the ring (no staging store), and the 24 window
+// registers are freed for occupancy.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+#ifndef FVB_RING_MINB
+#define FVB_RING_MINB 8
+#endif
+constexpr int kRingPD = 2;               // rows in flight ahead of the consumer
+constexpr int kRingRows = kRingPD + 3;   // ring slots
+
+template <int EQ, int FLUX, int RECON, int NT, bool FIN>
+__global__ void __launch_bounds__(NT, FVB_RING_MINB)
+ring_kernel(const StageParams p) {
+  constexpr int DIM = 2;
+  constexpr int NC = NComp<EQ, DIM>::value;
+  constexpr bool WENO = RECON != RECON_NONE;
+  constexpr int W = NT + 2;
+  extern __shared__ double smem[];
+  double* ring = smem;                               // [kRingRows][NC][W]
+  double* hx = ring + kRingRows * NC * W;            // [NC][NT]
+  double* lx = hx + (WENO ? NC * NT : 0);            // [NC][NT]
+  double* gx = lx + (WENO ? NC * NT : 0);            // [NC][NT]
+  double* nring = gx + NC * NT;                      // [3][NC][NT]: u^n rows for the RK combination
+  auto RG = [&](int slot, int c, int x) -> double& { return ring[(slot * NC + c) * W + x]; };
+  auto NR = [&](int slot, int c) -> double& { return nring[(slot * NC + c) * NT + threadIdx.x]; };
+
+  const int inst = blockIdx.z;
+  FvbState* st = p.st + (p.shared_state ? 0 : inst);
+  if (*(volatile int*)&st->done) return;
+  const double dt = p.kind == 0 ? 0.0 : *(volatile double*)&st->dt;
+  const double* __restrict__ us = p.us + p.origin + inst * p.si;
+  const double* un = p.un + p.origin + inst * p.si;
+  double* out = p.out + p.origin + inst * p.si;
+  const int tx = threadIdx.x;
+  const int64_t x0 = (int64_t)blockIdx.x * (NT - 2);
+  const int64_t xf = x0 - 1 + tx;
+  const bool cell = tx >= 1 && tx <= NT - 2 && xf < p.n[0];
+  const int64_t ra = (int64_t)blockIdx.y * p.H;
+  const int64_t rb = min(ra + (int64_t)p.H, p.n[1]);
+  const int64_t co = map_index(xf, p.n[0], p.bc[0], p.g);
+  // halo columns: thread 0 also copies x0-2, thread NT-1 also x0+NT-1
+  const bool halo_t = WENO && (tx == 0 || tx == NT - 1);
+  const int64_t hco = map_index(tx == 0 ? x0 - 2 : x0 + NT - 1, p.n[0], p.bc[0], p.g);
+  const int hcol = tx == 0 ? 0 : NT + 1;
+  auto roff = [&](int64_t r) -> int64_t { return map_index(r, p.n[1], p.bc[1], p.g) * p.sy; };
+  auto fetch = [&](int64_t r, int slot) {  // async copy of row r into a ring slot
+    const int64_t ro = roff(r);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, tx + 1), us + co + ro + c * p.sc);
+    if (halo_t) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, hcol), us + hco + ro + c * p.sc);
+    }
+  };
+
+  unsigned errb = 0;
+  double smax[DIM] = {0.0, 0.0};
+  double H[NC], G[NC], R[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) H[c] = G[c] = R[c] = 0.0;
+
+  // prologue: rows ra-2 .. ra-1+PD (slot of row r = (r - ra + 2) % kRingRows)
+  for (int k = 0; k < kRingPD + 2; ++k) {
+    fetch(ra - 2 + k, k);
+    cp_async_commit();
+  }
+  int sA = 0;  // slot of row r-1 at the top of the loop (r = ra-1 -> row ra-2)
+  for (int64_t r = ra - 1; r <= rb; ++r) {
+    const int sB = sA + 1 == kRingRows ? 0 : sA + 1;
+    const int sC = sB + 1 == kRingRows ? 0 : sB + 1;
+    // issue row r+1+PD into the slot that held row r-2 (free since last row),
+    // and u^n of row r+1 (consumed two iterations later) into its 3-slot ring
+    {
+      int sN = sC + kRingPD;  // slot(row) = (row - ra + 2) % kRingRows -> the slot of row r-2
+      sN = sN >= kRingRows ? sN - kRingRows : sN;
+      if (r + 1 + kRingPD <= rb + 1) fetch(r + 1 + kRingPD, sN);
+      if (p.kind >= 2 && cell && r + 1 >= ra && r + 1 < rb) {
+        const int64_t o = co + roff(r + 1);
+        const int ns = (int)((r + 1 - ra) % 3);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) cp_async8(&NR(ns, c), un + o + c * p.sc);
+      }
+      cp_async_commit();
+    }
+    cp_async_wait<kRingPD>();  // rows up to r+1 have landed (this thread's copies)
+    __syncthreads();           // ... and everybody's
+    const bool fin = cell && r - 1 >= ra;
+    double unc[NC];
+    if (fin && p.kind >= 2) {  // u^n of row r-1 landed with the group of iteration r-2
+      const int ns = (int)((r - 1 - ra) % 3);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) unc[c] = NR(ns, c);
+    }
+    if (cell) {  // march (y) direction: faces of row r, flux (r-1|r), finish row r-1
+      double A[NC], B[NC], C[NC], hi[NC], lo[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        A[c] = RG(sA, c, tx + 1);
+        B[c] = RG(sB, c, tx + 1);
+        C[c] = RG(sC, c, tx + 1);
+      }
+      weno_faces_nc<NC, RECON>(A, B, C, p.P.eps, hi, lo);
+      if (r >= ra) {
+        double GC[NC];
+        unsigned eb = 0;
+        interface_flux<EQ, FLUX, DIM, RECON>(H, lo, A, B, 1, p.P, GC, eb);
+        if (eb) errb |= 2u;
+        if (fin) {
+          double v[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+#if FVB_FAST
+            const double Lc = fma(G[c] - GC[c], p.id[1], R[c]);
+#else
+            const double Lc = R[c] - ddiv(GC[c] - G[c], p, 1);
+#endif
+            v[c] = rk_combine(p.kind, unc[c], A[c], dt, Lc);
+          }
+          const int64_t o = co + roff(r - 1);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
+          if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v, xf, r - 1, 0, smax);
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) G[c] = GC[c];
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) H[c] = hi[c];
+    }
+    if (r >= ra && r < rb) {  // in-plane (x) direction of row r, straight from the ring
+      if constexpr (EQ == EQ_EULER) {
+        if (p.check_input && cell) {
+          double B[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) B[c] = RG(sB, c, tx + 1);
+          if (!euler_physical<DIM>(B, p.P))
+            atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | flat_cell<DIM>(p, xf, r, 0));
+        }
+      }
+      if constexpr (WENO) {
+        double um[NC], uc[NC], up[NC], hi[NC], lo[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          um[c] = RG(sB, c, tx);
+          uc[c] = RG(sB, c, tx + 1);
+          up[c] = RG(sB, c, tx + 2);
+        }
+        weno_faces_nc<NC, RECON>(um, uc, up, p.P.eps, hi, lo);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          hx[c * NT + tx] = hi[c];
+          lx[c * NT + tx] = lo[c];
+        }
+        __syncthreads();
+      }
+      if (tx >= 1) {
+        double uL[NC], uR[NC], cl[NC], cr[NC], Gx[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          cl[c] = RG(sB, c, tx);
+          cr[c] = RG(sB, c, tx + 1);
+          if constexpr (WENO) {
+            uL[c] = hx[c * NT + tx - 1];
+            uR[c] = lx[c * NT + tx];
+          } else {
+            uL[c] = cl[c];
+            uR[c] = cr[c];
+          }
+        }
+        unsigned eb = 0;
+        interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 0, p.P, Gx, eb);
+        if (eb && xf <= p.n[0]) errb |= 1u;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) gx[c * NT + tx] = Gx[c];
+      }
+      __syncthreads();
+      if (cell) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+#if FVB_FAST
+          R[c] = (gx[c * NT + tx] - gx[c * NT + tx + 1]) * p.id[0];
+#else
+          R[c] = 0.0 - ddiv(gx[c * NT + tx + 1] - gx[c * NT + tx], p, 0);
+#endif
+        }
+      }
+    }
+    sA = sB;
+  }
+  cp_async_wait<0>();
+  if (errb) {
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+      if (errb & (1u << a))
+        atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | ((long long)(1 + a) << 40));
+  }
+  if constexpr (FIN) block_epilogue<DIM>(p, st, inst, smax, true);
+}
+
+template <int EQ, int RECON, int NT>
+constexpr int ring_smem_bytes() {
+  constexpr int NC = NComp<EQ, 2>::value;
+  return 8 * (kRingRows * NC * (NT + 2) + (RECON != RECON_NONE ? 2 : 0) * NC * NT + NC * NT + 3 * NC * NT);
+}
+
 // Standalone wave-speed pass: solver.py:128-136 (+ the initial is_physical
 // check of solver.py:211-212).  finalize = 1 also computes the first dt.
 template <int DIM, int EQ>
