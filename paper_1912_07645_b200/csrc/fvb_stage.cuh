@@ -380,11 +380,14 @@ struct TileCtx {
 #ifndef FVB_TILE_MINB
 #define FVB_TILE_MINB 8  // 2D: cap at 128 registers -> 16 warps/SM (measured best)
 #endif
+#ifndef FVB_TILE3_MINB
+#define FVB_TILE3_MINB 2  // 3D: 256-thread tile, cap at 128 registers -> 2 blocks/SM
+#endif
 #ifndef FVB_TILE_UNROLL
 #define FVB_TILE_UNROLL 1
 #endif
 template <int DIM, int EQ, int FLUX, int RECON, int NT, int NTY, bool FIN>
-__global__ void __launch_bounds__(NT * NTY, (DIM == 2 ? FVB_TILE_MINB : 1))
+__global__ void __launch_bounds__(NT * NTY, (DIM == 2 ? FVB_TILE_MINB : (DIM == 3 ? FVB_TILE3_MINB : 1)))
 stage_kernel(const StageParams p) {
   using T = TileCtx<DIM, EQ, FLUX, RECON, NT, NTY, FIN>;
   constexpr int NC = T::NC;
