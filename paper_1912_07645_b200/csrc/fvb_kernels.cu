@@ -11,7 +11,10 @@ namespace FVB_NS {
 template <int DIM> struct Blk;
 template <> struct Blk<1> { static constexpr int NT = 128, NTY = 1; };
 template <> struct Blk<2> { static constexpr int NT = 64, NTY = 1; };
-template <> struct Blk<3> { static constexpr int NT = 32, NTY = 8; };
+#ifndef FVB_TILE3_NTY
+#define FVB_TILE3_NTY 8
+#endif
+template <> struct Blk<3> { static constexpr int NT = 32, NTY = FVB_TILE3_NTY; };
 constexpr int kStripWarps = 4;
 
 // cells per block along x (reported as nt-2) and the y tile (nty-2, 3D only)

@@ -793,6 +793,9 @@ ring_kernel(const StageParams p) {
   for (int64_t r = ra - 1; r <= rb; ++r) {
     const int sB = sA + 1 == kRingRows ? 0 : sA + 1;
     const int sC = sB + 1 == kRingRows ? 0 : sB + 1;
+    // iteration ra-1 has no in-plane barrier: make sure its reads of the
+    // slot about to be refilled (row ra-2) are done
+    if (r == ra) __syncthreads();
     // issue row r+1+PD into the slot that held row r-2 (free since last row),
     // and u^n of row r+1 (consumed two iterations later) into its 3-slot ring
     {
