@@ -812,14 +812,19 @@ ring_kernel(const StageParams p) {
     }
     cp_async_wait<kRingPD>();  // rows up to r+1 have landed (this thread's copies)
     __syncthreads();           // ... and everybody's
+    // Every lane computes (the two halo lanes on real neighbour columns), only
+    // side effects are predicated on `cell`: no divergent regions, so no
+    // reconvergence bookkeeping in the hot loop.
     const bool fin = cell && r - 1 >= ra;
     double unc[NC];
-    if (fin && p.kind >= 2) {  // u^n of row r-1 landed with the group of iteration r-2
+#pragma unroll
+    for (int c = 0; c < NC; ++c) unc[c] = 0.0;
+    if (p.kind >= 2 && r - 1 >= ra) {  // u^n of row r-1 landed with the group of iteration r-2
       const int ns = (int)((r - 1 - ra) % 3);
 #pragma unroll
       for (int c = 0; c < NC; ++c) unc[c] = NR(ns, c);
     }
-    if (cell) {  // march (y) direction: faces of row r, flux (r-1|r), finish row r-1
+    {  // march (y) direction: faces of row r, flux (r-1|r), finish row r-1
       double A[NC], B[NC], C[NC], hi[NC], lo[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
@@ -832,18 +837,18 @@ ring_kernel(const StageParams p) {
         double GC[NC];
         unsigned eb = 0;
         interface_flux<EQ, FLUX, DIM, RECON>(H, lo, A, B, 1, p.P, GC, eb);
-        if (eb) errb |= 2u;
-        if (fin) {
-          double v[NC];
+        if (eb && cell) errb |= 2u;
+        double v[NC];
 #pragma unroll
-          for (int c = 0; c < NC; ++c) {
+        for (int c = 0; c < NC; ++c) {
 #if FVB_FAST
-            const double Lc = fma(G[c] - GC[c], p.id[1], R[c]);
+          const double Lc = fma(G[c] - GC[c], p.id[1], R[c]);
 #else
-            const double Lc = R[c] - ddiv(GC[c] - G[c], p, 1);
+          const double Lc = R[c] - ddiv(GC[c] - G[c], p, 1);
 #endif
-            v[c] = rk_combine(p.kind, unc[c], A[c], dt, Lc);
-          }
+          v[c] = rk_combine(p.kind, unc[c], A[c], dt, Lc);
+        }
+        if (fin) {
           const int64_t o = co + roff(r - 1);
 #pragma unroll
           for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
@@ -881,14 +886,15 @@ ring_kernel(const StageParams p) {
         }
         __syncthreads();
       }
-      if (tx >= 1) {
+      {  // x interface tx sits between face cells tx-1 and tx (lane 0's is unused)
+        const int tl = tx >= 1 ? tx - 1 : 0;
         double uL[NC], uR[NC], cl[NC], cr[NC], Gx[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           cl[c] = RG(sB, c, tx);
           cr[c] = RG(sB, c, tx + 1);
           if constexpr (WENO) {
-            uL[c] = hx[c * NT + tx - 1];
+            uL[c] = hx[c * NT + tl];
             uR[c] = lx[c * NT + tx];
           } else {
             uL[c] = cl[c];
@@ -897,18 +903,19 @@ ring_kernel(const StageParams p) {
         }
         unsigned eb = 0;
         interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 0, p.P, Gx, eb);
-        if (eb && xf <= p.n[0]) errb |= 1u;
+        if (eb && tx >= 1 && xf <= p.n[0]) errb |= 1u;
 #pragma unroll
         for (int c = 0; c < NC; ++c) gx[c * NT + tx] = Gx[c];
       }
       __syncthreads();
-      if (cell) {
+      {
+        const int tr = tx + 1 < NT ? tx + 1 : NT - 1;
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
 #if FVB_FAST
-          R[c] = (gx[c * NT + tx] - gx[c * NT + tx + 1]) * p.id[0];
+          R[c] = (gx[c * NT + tx] - gx[c * NT + tr]) * p.id[0];
 #else
-          R[c] = 0.0 - ddiv(gx[c * NT + tx + 1] - gx[c * NT + tx], p, 0);
+          R[c] = 0.0 - ddiv(gx[c * NT + tr] - gx[c * NT + tx], p, 0);
 #endif
         }
       }
