@@ -31,7 +31,7 @@ static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
   if constexpr (DIM == 2) {
     if (p.variant == 2) {
       constexpr int NT = Blk<2>::NT;
-      constexpr int smem = ring_smem_bytes<EQ, RECON, NT>();
+      const int smem = ring_smem_bytes<EQ, RECON, NT>() + 8 * (p.H + kRingPD + 4);  // + row-offset table
       ring_kernel<EQ, FLUX, RECON, NT, FIN><<<grid, NT, smem, s>>>(p);
       return 0;
     }

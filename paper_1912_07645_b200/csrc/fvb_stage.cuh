@@ -767,7 +767,11 @@ ring_kernel(const StageParams p) {
   const bool halo_t = WENO && (tx == 0 || tx == NT - 1);
   const int64_t hco = map_index(tx == 0 ? x0 - 2 : x0 + NT - 1, p.n[0], p.bc[0], p.g);
   const int hcol = tx == 0 ? 0 : NT + 1;
-  auto roff = [&](int64_t r) -> int64_t { return map_index(r, p.n[1], p.bc[1], p.g) * p.sy; };
+  // row offsets of rows ra-2 .. rb+PD+1, computed once per block
+  int64_t* rtab = reinterpret_cast<int64_t*>(nring + 3 * NC * NT);
+  for (int i = tx; i < p.H + kRingPD + 4; i += NT) rtab[i] = map_index(ra - 2 + i, p.n[1], p.bc[1], p.g) * p.sy;
+  __syncthreads();
+  auto roff = [&](int64_t r) -> int64_t { return rtab[r - (ra - 2)]; };
   auto fetch = [&](int64_t r, int slot) {  // async copy of row r into a ring slot
     const int64_t ro = roff(r);
 #pragma unroll
@@ -780,6 +784,9 @@ ring_kernel(const StageParams p) {
 
   unsigned errb = 0;
   double smax[DIM] = {0.0, 0.0};
+  // RK stage as a*u^n + b*(u^s + dt L) (solver.py:166-173); fast mode only
+  const double rk_a = p.kind == 2 ? 0.5 : (p.kind == 3 ? 0.75 : (p.kind == 4 ? 1.0 / 3.0 : 0.0));
+  const double rk_b = p.kind == 2 ? 0.5 : (p.kind == 3 ? 0.25 : (p.kind == 4 ? 2.0 / 3.0 : 1.0));
   double H[NC], G[NC], R[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) H[c] = G[c] = R[c] = 0.0;
@@ -846,7 +853,11 @@ ring_kernel(const StageParams p) {
 #else
           const double Lc = R[c] - ddiv(GC[c] - G[c], p, 1);
 #endif
+#if FVB_FAST
+          v[c] = p.kind == 0 ? Lc : fma(rk_a, unc[c], rk_b * fma(dt, Lc, A[c]));
+#else
           v[c] = rk_combine(p.kind, unc[c], A[c], dt, Lc);
+#endif
         }
         if (fin) {
           const int64_t o = co + roff(r - 1);
