@@ -340,20 +340,26 @@ struct TileCtx {
   __device__ __forceinline__ void row(int64_t r, double* A, const double* B, const double* C, double* H, double* G,
                                       double* R) {
     const bool fin = cell && r - 1 >= ra;
+    // every lane of a warp that holds cells computes (halo lanes on real
+    // neighbour columns); only side effects are predicated on `cell`.  Whole
+    // halo warps (3D: ty = 0, NTY-1) skip the march work.
+    const bool active = !PY || (ty >= 1 && ty <= NTY - 2);
     double unc[NC];
-    if (fin && p.kind >= 2) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) unc[c] = 0.0;
+    if (active && r - 1 >= ra && p.kind >= 2) {
       const int64_t o = co + roff(r - 1);
 #pragma unroll
       for (int c = 0; c < NC; ++c) unc[c] = un[o + c * p.sc];
     }
-    if (cell) {
+    if (active) {
       double hi[NC], lo[NC];
       weno_faces_nc<NC, RECON>(A, B, C, p.P.eps, hi, lo);
       if (r >= ra) {
         double GC[NC];
         unsigned eb = 0;
         interface_flux<EQ, FLUX, DIM, RECON>(H, lo, A, B, MA, p.P, GC, eb);
-        if (eb) errb |= 1u << MA;
+        if (eb && cell) errb |= 1u << MA;
         if (fin) {
           double Lc[NC];
 #pragma unroll
