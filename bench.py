@@ -202,7 +202,7 @@ def bench_ours(args, ws, rank, local):
 
     # roofline: the 3 fused stage launches of a step (the only kernels in it)
     bytes_step = cells * 8 * ncomp * (2 + 3 + 3)  # stage1: r us, w out; stages 2-3: r us, un, w out
-    kname = {"kh2d": "stage_kernel<2,EULER,HLLC,WENO2>", "mc": "stage_kernel<2,EULER,HLLC,WENO2> (batched)",
+    kname = {"kh2d": "ring_kernel<EULER,HLLC,WENO2>", "mc": "ring_kernel<EULER,HLLC,WENO2> (batched)",
              "kh3d": "stage_kernel<3,EULER,HLLC,WENO2>"}[args.config]
     peak, peak_src = _hbm_peak()
     achieved = bytes_step / (ms_per_step * 1e-3) / 1e9
