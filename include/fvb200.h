@@ -173,6 +173,11 @@ int fvb_run_set_topology(fvb_ctx* ctx, const int32_t* ranks, const int32_t* peri
  * Stage inputs: stage s of RK2/3 reads bufs[s]; RK1 reads bufs[steps % 2]. */
 int fvb_run_set_external_reduce(fvb_ctx* ctx, int on);
 int fvb_run_stage(fvb_ctx* ctx, int stage);
+/* the same stage restricted to march-axis cells [row_lo, row_hi) (dim >= 2):
+ * the inner box runs while the march-axis halos are in flight, the shell
+ * slabs after they land (overlapped_residual, parallel.py:288-361); pass
+ * last_part = 1 on the final call of a stage */
+int fvb_run_stage_rows(fvb_ctx* ctx, int stage, int64_t row_lo, int64_t row_hi, int last_part);
 int fvb_run_export(fvb_ctx* ctx, double* d_out);
 int fvb_run_finalize(fvb_ctx* ctx, const double* d_global, int post);
 /* kernel launches issued by the last fvb_run / fvb_run_steps calls */

@@ -173,7 +173,7 @@ static StageParams base_params(const fvb_scheme& s, const fvb_layout& L) {
 }
 
 // Grid of the stage kernel; fills chunks / H / nblocks.
-static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst) {
+static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t row_lo = 0, int64_t row_hi = -1) {
   int nt, nty;
   const char* kv = getenv("FVB_KERNEL");
   // 2D default: the cp.async ring kernel (fastest measured);
@@ -189,7 +189,11 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst) {
   g.x = (unsigned)strips;
   int64_t H = 1, chunks = 1;
   if (s.dim >= 2) {
-    const int64_t nm = p.n[s.dim - 1];
+    const int64_t n_march = p.n[s.dim - 1];
+    if (row_hi < 0) row_hi = n_march;
+    p.row_lo = row_lo;
+    p.row_hi = row_hi;
+    const int64_t nm = std::max<int64_t>(1, row_hi - row_lo);
     int64_t ytiles = 1;
     if (s.dim == 3) ytiles = (p.n[1] + (nty - 2) - 1) / (nty - 2);
     // aim for ~2 waves of resident blocks over 148 SMs
@@ -216,6 +220,8 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst) {
     }
   } else {
     g.z = ninst;
+    p.row_lo = 0;
+    p.row_hi = 1;
   }
   p.H = (int)H;
   p.chunks = (int)chunks;
@@ -675,6 +681,26 @@ int fvb_run_stage(fvb_ctx* ctx, int stage) {
   int r = do_stage(ctx, P.s, p, P.grid);
   if (r) return r;
   if (stage == P.nstages - 1) P.steps_enqueued++;
+  return FVB_OK;
+}
+
+int fvb_run_stage_rows(fvb_ctx* ctx, int stage, int64_t row_lo, int64_t row_hi, int last_part) {
+  RunPlan& P = ctx->plan;
+  if (!P.active || !P.external) return set_err(ctx, FVB_E_CONFIG, "fvb_run_stage_rows needs an external-reduce run");
+  if (stage < 0 || stage >= P.nstages) return set_err(ctx, FVB_E_CONFIG, "stage %d out of range", stage);
+  if (P.s.dim < 2) return set_err(ctx, FVB_E_CONFIG, "row ranges need a march axis (dim >= 2)");
+  StageParams p = P.stage[stage];
+  if (P.s.rk_order == 1) {
+    const int par = (int)(P.steps_enqueued & 1);
+    p.us = P.bufs[par];
+    p.un = P.bufs[par];
+    p.out = P.bufs[1 - par];
+  }
+  if (row_hi <= row_lo) return FVB_OK;
+  dim3 g = stage_grid(P.s, p, P.ninst, row_lo, row_hi);
+  int r = do_stage(ctx, P.s, p, g);
+  if (r) return r;
+  if (last_part && stage == P.nstages - 1) P.steps_enqueued++;
   return FVB_OK;
 }
 

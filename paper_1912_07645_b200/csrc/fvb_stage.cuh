@@ -420,8 +420,8 @@ stage_kernel(const StageParams p) {
   const int64_t yf = T::PY ? y0 - 1 + ty : 0;
   bool cell = tx >= 1 && tx <= NT - 2 && xf < p.n[0];
   if (T::PY) cell = cell && ty >= 1 && ty <= NTY - 2 && yf < p.n[1];
-  const int64_t ra = T::MARCH ? (int64_t)chunk * p.H : 0;
-  const int64_t rb = T::MARCH ? min(ra + (int64_t)p.H, p.n[T::MA]) : 1;
+  const int64_t ra = T::MARCH ? p.row_lo + (int64_t)chunk * p.H : 0;
+  const int64_t rb = T::MARCH ? min(ra + (int64_t)p.H, p.row_hi) : 1;
   T t{p, st, p.us + p.origin + inst * p.si, p.un + p.origin + inst * p.si, p.out + p.origin + inst * p.si, smem,
       p.kind == 0 ? 0.0 : *(volatile double*)&st->dt, tx, ty, x0, y0, xf, yf, cell, ra, rb, 0, 0u, {}};
   t.co = t.pin(xf, yf);
@@ -689,8 +689,8 @@ strip_kernel(const StageParams p) {
         s.finish(0, B, unc, res);
       }
     } else {
-      s.ra = (int64_t)blockIdx.y * p.H;
-      s.rb = min(s.ra + (int64_t)p.H, p.n[1]);
+      s.ra = p.row_lo + (int64_t)blockIdx.y * p.H;
+      s.rb = min(s.ra + (int64_t)p.H, p.row_hi);
       double W0[NC], W1[NC], W2[NC], H[NC], G[NC], R[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) H[c] = G[c] = R[c] = 0.0;
@@ -766,8 +766,8 @@ ring_kernel(const StageParams p) {
   const int64_t x0 = (int64_t)blockIdx.x * (NT - 2);
   const int64_t xf = x0 - 1 + tx;
   const bool cell = tx >= 1 && tx <= NT - 2 && xf < p.n[0];
-  const int64_t ra = (int64_t)blockIdx.y * p.H;
-  const int64_t rb = min(ra + (int64_t)p.H, p.n[1]);
+  const int64_t ra = p.row_lo + (int64_t)blockIdx.y * p.H;
+  const int64_t rb = min(ra + (int64_t)p.H, p.row_hi);
   const int64_t co = map_index(xf, p.n[0], p.bc[0], p.g);
   // halo columns: thread 0 also copies x0-2, thread NT-1 also x0+NT-1
   const bool halo_t = WENO && (tx == 0 || tx == NT - 1);

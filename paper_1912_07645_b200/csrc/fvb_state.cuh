@@ -188,6 +188,8 @@ struct StageParams {
   int stage_idx;      // stage number within the step (error ordering)
   int chunks;         // chunks along the march axis
   int H;              // rows per chunk
+  int64_t row_lo;     // march-axis cell range computed by this launch: [row_lo, row_hi)
+  int64_t row_hi;     // (inner box / shell slabs of the overlap schedule, parallel.py:288-361)
   unsigned nblocks;   // blocks per state (finalize counter)
   int shared_state;   // 1: all instances are subdomains of one run (one FvbState)
   int defer_finalize; // 1: leave maxima/flags in the state; the caller reduces them

@@ -287,7 +287,7 @@ def run_parallel(init, cfg, ranks_per_axis, n_steps: int | None = None, overlap:
     if torch.distributed.is_available() and torch.distributed.is_initialized() \
             and torch.distributed.get_world_size() == topo.size and topo.size > 1:
         cpu = torch.distributed.get_backend() == "gloo"
-        return run_parallel_nccl(init, cfg, topo, parts, n_steps, arith=arith, cpu_comm=cpu)
+        return run_parallel_nccl(init, cfg, topo, parts, n_steps, arith=arith, cpu_comm=cpu, overlap=overlap)
     locals_ = scatter_field(init, parts)
     grid = parts[0].grid
     ncomp = init.ncomp
@@ -325,21 +325,21 @@ def run_parallel(init, cfg, ranks_per_axis, n_steps: int | None = None, overlap:
     return stitch_fields(init.grid, parts, finals), [list(recs) for _ in range(topo.size)]
 
 
-def halo_exchange_dist(topo: RankTopology, rank: int, periodic, pack, unpack, alloc, dist, group=None):
-    """Face-only halo exchange of one rank over torch.distributed P2P
-    (NCCL on GPUs; gloo in the CPU tests).
+def start_halo_exchange(topo: RankTopology, rank: int, periodic, pack, alloc, dist, group=None, axes=None):
+    """Post the face-only halo sends/receives of one rank over
+    torch.distributed P2P (NCCL on GPUs; gloo in the CPU tests) and return
+    a handle for ``finish_halo_exchange``.
 
     ``pack(axis, side)`` returns the contiguous slab of the g interior layers
-    next to face (axis, side); ``alloc(axis)`` an empty receive buffer;
-    ``unpack(axis, side, buf)`` writes a received slab into the ghosts of
-    that face.  Axes are exchanged concurrently (the
-    residual never reads corner ghosts, solver.py:99-104).  Ordering rule so
-    that a pair of ranks that are mutual neighbours on both sides (2 ranks on
-    a periodic axis, parallel.py:227-230) match: sends are issued by side
-    (low, high), receives by the SENDER's side, i.e. high ghosts first.
-    World-edge sides without a neighbour are left to the caller (outflow)."""
+    next to face (axis, side); ``alloc(axis)`` an empty receive buffer.  Axes
+    are exchanged concurrently (the residual never reads corner ghosts,
+    solver.py:99-104).  Ordering rule so that a pair of ranks that are
+    mutual neighbours on both sides (2 ranks on a periodic axis,
+    parallel.py:227-230) match: sends are issued by side (low, high),
+    receives by the SENDER's side, i.e. high ghosts first.  World-edge sides
+    without a neighbour are left to the caller (outflow)."""
     ops, recvs = [], []
-    for axis in range(topo.dim):
+    for axis in (range(topo.dim) if axes is None else axes):
         if topo.ranks_per_axis[axis] == 1:
             continue
         nb = [topo.neighbor(rank, axis, side, bool(periodic[axis])) for side in (0, 1)]
@@ -351,14 +351,25 @@ def halo_exchange_dist(topo: RankTopology, rank: int, periodic, pack, unpack, al
                 buf = alloc(axis)
                 ops.append(dist.P2POp(dist.irecv, buf, nb[side], group))
                 recvs.append((axis, side, buf))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+    reqs = dist.batch_isend_irecv(ops) if ops else []
+    return reqs, recvs
+
+
+def finish_halo_exchange(handle, unpack):
+    reqs, recvs = handle
+    for req in reqs:
+        req.wait()
     for axis, side, buf in recvs:
         unpack(axis, side, buf)
 
 
-def run_parallel_nccl(init, cfg, topo, parts, n_steps, *, arith=None, group=None, cpu_comm: bool = False):
+def halo_exchange_dist(topo: RankTopology, rank: int, periodic, pack, unpack, alloc, dist, group=None, axes=None):
+    """Blocking face-only halo exchange (start + finish)."""
+    finish_halo_exchange(start_halo_exchange(topo, rank, periodic, pack, alloc, dist, group, axes), unpack)
+
+
+def run_parallel_nccl(init, cfg, topo, parts, n_steps, *, arith=None, group=None, cpu_comm: bool = False,
+                      overlap: bool = True):
     """One subdomain per process (rank r of the torch.distributed group owns
     part r), stage-wise: halo exchange of every stage input, fused stage
     kernel, then one all-reduce(MAX) of [maxima, error flags] per step and a
@@ -399,7 +410,7 @@ def run_parallel_nccl(init, cfg, topo, parts, n_steps, *, arith=None, group=None
             dist.all_reduce(red, op=dist.ReduceOp.MAX, group=group)
         ctx.check(ctx.lib.fvb_run_finalize(ctx.h, N.C.c_void_p(red.data_ptr()), post))
 
-    def exchange(u):
+    def movers(u):
         ptr = N.C.c_void_p(u.data_ptr())
 
         def alloc(axis):
@@ -418,13 +429,40 @@ def run_parallel_nccl(init, cfg, topo, parts, n_steps, *, arith=None, group=None
             ctx.check(ctx.lib.fvb_halo_unpack(ctx.h, N.C.byref(s), N.C.byref(L), ptr, axis, side,
                                               N.C.c_void_p(b.data_ptr())))
 
-        halo_exchange_dist(topo, rank, periodic, pack, unpack, alloc, dist, group)
+        return pack, unpack, alloc
+
+    def outflow_edges(u, axes):
         # world edges of split, non-periodic axes: outflow ghosts (parallel.py:246-247)
         view = DeviceField(grid, ncomp, u[0])
-        for axis in split:
+        for axis in axes:
             for side in (0, 1):
                 if topo.neighbor(rank, axis, side, bool(periodic[axis])) is None:
                     _fill_one_side(view, axis, side)
+
+    march = grid.dim - 1
+    g = grid.ghost_width
+    n_march = grid.cells[march] if grid.dim >= 2 else 0
+    # overlap schedule (overlapped_residual, parallel.py:325-361): the
+    # march-axis halos travel while the inner box [g, n-g) is computed
+    ovl = overlap and grid.dim >= 2 and march in split and n_march > 2 * g
+
+    def stage(st, u):
+        pack, unpack, alloc = movers(u)
+        if not ovl:
+            halo_exchange_dist(topo, rank, periodic, pack, unpack, alloc, dist, group)
+            outflow_edges(u, split)
+            ctx.check(ctx.lib.fvb_run_stage(ctx.h, st))
+            return
+        other = [a for a in split if a != march]
+        if other:
+            halo_exchange_dist(topo, rank, periodic, pack, unpack, alloc, dist, group, axes=other)
+            outflow_edges(u, other)
+        handle = start_halo_exchange(topo, rank, periodic, pack, alloc, dist, group, axes=[march])
+        ctx.check(ctx.lib.fvb_run_stage_rows(ctx.h, st, g, n_march - g, 0))      # inner box
+        finish_halo_exchange(handle, unpack)
+        outflow_edges(u, [march])
+        ctx.check(ctx.lib.fvb_run_stage_rows(ctx.h, st, 0, g, 0))                # shell slabs
+        ctx.check(ctx.lib.fvb_run_stage_rows(ctx.h, st, n_march - g, n_march, 1))
 
     reduce_and_finalize(0)
     nst = 1 if cfg.rk_order == 1 else cfg.rk_order
@@ -434,8 +472,7 @@ def run_parallel_nccl(init, cfg, topo, parts, n_steps, *, arith=None, group=None
             break
         tic = time.perf_counter()
         for st in range(nst):
-            exchange(bufs[int(infos[0].steps) % 2] if nst == 1 else bufs[st])
-            ctx.check(ctx.lib.fvb_run_stage(ctx.h, st))
+            stage(st, bufs[int(infos[0].steps) % 2] if nst == 1 else bufs[st])
         reduce_and_finalize(1)
         infos, _ = run.poll()
         run.read_log(infos, time.perf_counter() - tic)

@@ -20,7 +20,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, name, lay, n_steps, out):
+def _worker(rank, world, port, name, lay, n_steps, overlap, out):
     import json
     from pathlib import Path
 
@@ -41,7 +41,7 @@ def _worker(rank, world, port, name, lay, n_steps, out):
     grid, cfg = product_objects(case["scheme"])
     data = np.array(arrays[name + "__init"])
     init = P.Field(grid, data.shape[0], data)
-    res, recs = run_parallel(init, cfg, lay, n_steps=n_steps, arith="exact")
+    res, recs = run_parallel(init, cfg, lay, n_steps=n_steps, overlap=overlap, arith="exact")
     if rank == 0:
         sc = oracle_scheme(case["scheme"])
         if n_steps is None:
@@ -55,14 +55,19 @@ def _worker(rank, world, port, name, lay, n_steps, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,lay,n_steps", [("kh2d64_weno2_50", (2, 1), 4),
-                                              ("euler2d_hllc_weno3_outflow", (2, 2), 3),
-                                              ("burgers1d_weno2_rk1_periodic", (2,), 7),
-                                              ("burgers1d_weno3_rk3_outflow", (2,), None)])
-def test_run_parallel_process_per_rank(name, lay, n_steps):
+@pytest.mark.parametrize("name,lay,n_steps,overlap", [
+    ("kh2d64_weno2_50", (2, 1), 4, True),
+    ("kh2d64_weno2_50", (1, 2), 4, True),     # march axis split: inner box overlaps the exchange
+    ("kh2d64_weno2_50", (1, 2), 4, False),
+    ("euler2d_hllc_weno3_outflow", (2, 2), 3, True),
+    ("burgers1d_weno2_rk1_periodic", (2,), 7, True),
+    ("burgers1d_weno3_rk3_outflow", (2,), None, True),
+    ("kh3d16_weno2_5", (1, 1, 2), 2, True),
+    ("euler3d_hllc_none_outflow", (1, 2, 2), 3, True)])
+def test_run_parallel_process_per_rank(name, lay, n_steps, overlap):
     world = int(np.prod(lay))
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _port(), name, lay, n_steps, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _port(), name, lay, n_steps, overlap, out), nprocs=world, join=True)
     assert out.get("ok"), (name, lay)
     assert out["recs"] == world
