@@ -134,6 +134,7 @@ class Context:
 
     def __init__(self, device: int = 0, stream=None):
         _require_cuda()
+        tune_host_malloc()
         import torch
 
         self.lib = load_library()
@@ -209,6 +210,20 @@ def context(device: int | None = None) -> Context:
             ctx = Context(device, stream)
             _ctx_cache[key] = ctx
         return ctx
+
+
+def tune_host_malloc() -> None:
+    """Keep large host allocations (result fields) in the malloc heap instead
+    of fresh mmaps, so repeated results reuse already-faulted pages
+    (FVB_MALLOPT=1)."""
+    if os.environ.get("FVB_MALLOPT", "1") != "1":
+        return
+    try:
+        libc = C.CDLL("libc.so.6")
+        libc.mallopt(-3, 1 << 30)  # M_MMAP_THRESHOLD
+        libc.mallopt(-1, 1 << 31)  # M_TRIM_THRESHOLD
+    except OSError:
+        pass
 
 
 def default_arith() -> str:
