@@ -199,7 +199,7 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
     // aim for ~2 waves of resident blocks over 148 SMs
     // resident blocks per SM (register-limited) and waves of blocks: one
     // wave keeps the march long (fewer redundant halo rows per chunk)
-    int64_t per_sm = s.dim == 3 ? 2 : (p.variant == 0 ? 4 : 8);
+    int64_t per_sm = s.dim == 3 ? 2 : (p.variant == 0 ? 4 : 512 / nt);  // 16 warps/SM at 128 registers
     int64_t waves = 1;
     if (const char* e = getenv("FVB_BLOCKS_PER_SM")) per_sm = std::max(1, atoi(e));
     if (const char* e = getenv("FVB_WAVES")) waves = std::max(1, atoi(e));

@@ -16,10 +16,15 @@ template <> struct Blk<2> { static constexpr int NT = 64, NTY = 1; };
 #endif
 template <> struct Blk<3> { static constexpr int NT = 32, NTY = FVB_TILE3_NTY; };
 constexpr int kStripWarps = 4;
+#ifndef FVB_RING_NT
+#define FVB_RING_NT 64
+#endif
+constexpr int kRingNT = FVB_RING_NT;
 
 // cells per block along x (reported as nt-2) and the y tile (nty-2, 3D only)
 void stage_block(int dim, int variant, int& nt, int& nty) {
   if (dim == 1 && variant == 2) variant = 1;
+  if (dim == 2 && variant == 2) { nt = kRingNT; nty = 1; return; }
   if (dim <= 2 && variant == 0) { nt = kStripCells * kStripWarps + 2; nty = 1; }
   else if (dim == 1) { nt = Blk<1>::NT; nty = 1; }
   else if (dim == 2) { nt = Blk<2>::NT; nty = 1; }
@@ -30,7 +35,7 @@ template <int DIM, int EQ, int FLUX, int RECON, bool FIN>
 static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
   if constexpr (DIM == 2) {
     if (p.variant == 2) {
-      constexpr int NT = Blk<2>::NT;
+      constexpr int NT = kRingNT;
       const int smem = ring_smem_bytes<EQ, RECON, NT>() + 8 * (p.H + kRingPD + 4);  // + row-offset table
       ring_kernel<EQ, FLUX, RECON, NT, FIN><<<grid, NT, smem, s>>>(p);
       return 0;

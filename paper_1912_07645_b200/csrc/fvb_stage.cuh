@@ -725,6 +725,13 @@ strip_kernel(const StageParams p) {
 // row straight from the ring (no staging store), and the 24 window
 // registers are freed for occupancy.
 // ---------------------------------------------------------------------------
+#ifndef FVB_RING_NT_FOR_MINB
+#ifdef FVB_RING_NT
+#define FVB_RING_NT_FOR_MINB FVB_RING_NT
+#else
+#define FVB_RING_NT_FOR_MINB 64
+#endif
+#endif
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
@@ -734,7 +741,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 #ifndef FVB_RING_MINB
-#define FVB_RING_MINB 8
+#define FVB_RING_MINB (512 / FVB_RING_NT_FOR_MINB)
 #endif
 constexpr int kRingPD = 2;               // rows in flight ahead of the consumer
 constexpr int kRingRows = kRingPD + 3;   // ring slots

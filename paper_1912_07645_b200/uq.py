@@ -353,14 +353,18 @@ def gather_ordered(tensors, count: int, dist, group, world):
     ranks in rank order -- the order run_mc merges samples in."""
     import torch
 
-    cnt = torch.tensor([int(count)], dtype=torch.int64, device=tensors[0].device)
+    dev = tensors[0].device
+    # gloo moves host tensors only: stage device data through host memory
+    host = dist.get_backend(group) == "gloo" and dev.type == "cuda"
+    cnt = torch.tensor([int(count)], dtype=torch.int64, device="cpu" if host else dev)
     cnts = [torch.zeros_like(cnt) for _ in range(world)]
     dist.all_gather(cnts, cnt, group=group)
     gathered = []
     for t in tensors:
-        parts = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(parts, t.contiguous(), group=group)
-        gathered.append(parts)
+        src = t.contiguous().cpu() if host else t.contiguous()
+        parts = [torch.empty_like(src) for _ in range(world)]
+        dist.all_gather(parts, src, group=group)
+        gathered.append([x.to(dev) for x in parts] if host else parts)
     return [(int(cnts[r].item()), [g[r] for g in gathered]) for r in range(world)]
 
 
