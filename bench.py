@@ -147,6 +147,9 @@ def bench_ours(args, ws, rank, local):
         b0 = torch.from_numpy(np.stack([f.data for f in inits])).to("cuda")
     else:
         init = kelvin_helmholtz(grid, KH_VECTOR)
+        if args.state_file and Path(args.state_file).exists():
+            init = P.Field(grid, dim + 2, np.load(args.state_file))  # developed state saved by tools/make_state.py
+            args.warm_time = 0.0
         b0 = DeviceField.from_host(init).data
     bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
     total_steps = args.warmup + args.steps
@@ -341,6 +344,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sustain", type=float, default=1.5, help="seconds of untimed load for the clock sampler")
     ap.add_argument("--warm-time", type=float, default=1.0, help="simulated time reached before timing")
+    ap.add_argument("--state-file", default=None, help="start from a saved developed state (profiling)")
     args = ap.parse_args()
     if args.cells is None:
         args.cells = {"kh2d": N_CELLS, "mc": 512, "kh3d": 256}[args.config]

@@ -35,6 +35,13 @@ __device__ __forceinline__ double np_max(double a, double b) { return (a > b || 
 __device__ __forceinline__ double np_min(double a, double b) { return (a < b || a != a) ? a : b; }
 #endif
 
+// Bitwise equality on the integer pipes (keeps warp-shortcut tests off the
+// FP64 pipe).  It is conservative: +0/-0 count as different, so such lanes
+// simply take the general path, whose own numeric tests decide.
+__device__ __forceinline__ bool bit_eq(double a, double b) {
+  return __double_as_longlong(a) == __double_as_longlong(b);
+}
+
 #if FVB_FAST
 // 1/x: MUFU seed + two Newton steps (full double precision for normal x)
 __device__ __forceinline__ double frcp(double x) {
@@ -51,12 +58,14 @@ __device__ __forceinline__ double fdiv(double a, double b) {
   const double q = a * r;
   return fma(fma(-b, q, a), r, q);
 }
-// sqrt(x), x > 0: rsqrt seed + Newton, final residual correction
+// sqrt(x), x > 0: rsqrt seed (~1e-6) + one Newton step on 1/sqrt (~1e-12),
+// then one residual correction of s = x*y.  Measured on the B200
+// (tools/mufu_precision.cu): equal to the correctly rounded sqrt for 4M
+// log-uniform samples over [e^-20, e^20].
 __device__ __forceinline__ double fsqrt(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
   y = y * fma(-hx * y, y, 1.5);
   double s = x * y;
   return fma(fma(-s, s, x), 0.5 * y, s);  // x > 0 on every physical state
@@ -199,16 +208,66 @@ __device__ __forceinline__ void weno_faces_nc(const double* um, const double* uc
 #pragma unroll
     for (int c = 0; c < NC; ++c) { hi[c] = uc[c]; lo[c] = uc[c]; }
   } else {
+    // hi = uc + dh, lo = uc - dl.  A warp whose every stencil is flat
+    // (D0 = D1 = +0 in all components) skips the weights: the formula then
+    // gives dh = dl = +0 exactly in both modes (signed zeros included).
+    double dh[NC], dl[NC];
     bool flat = true;
 #pragma unroll
-    for (int c = 0; c < NC; ++c) flat &= (uc[c] == um[c]) & (up[c] == uc[c]);
-    if (!__any_sync(__activemask(), !flat)) {
+    for (int c = 0; c < NC; ++c) {
+      flat &= bit_eq(uc[c], um[c]) & bit_eq(up[c], uc[c]);
+      dh[c] = 0.0;
+      dl[c] = 0.0;
+    }
+    if (__any_sync(__activemask(), !flat)) {
+      double D0[NC], D1[NC];
 #pragma unroll
-      for (int c = 0; c < NC; ++c) { hi[c] = uc[c] + 0.0; lo[c] = uc[c] - 0.0; }
-      return;
+      for (int c = 0; c < NC; ++c) {
+        D0[c] = uc[c] - um[c];
+        D1[c] = up[c] - uc[c];
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+#if FVB_FAST
+        const double e0 = fma(D0[c], D0[c], eps);
+        const double e1 = fma(D1[c], D1[c], eps);
+        const double q0 = e0 * e0;
+        const double q1 = e1 * e1;
+        if constexpr (RECON == RECON_WENO2) {
+          dh[c] = (0.5 * frcp(q0 + q1)) * fma(q1, D0[c], q0 * D1[c]);
+          dl[c] = dh[c];
+        } else {
+          dh[c] = 0.5 * (fma(q1, D0[c], 2.0 * q0 * D1[c]) * frcp(fma(2.0, q0, q1)));
+          dl[c] = 0.5 * (fma(q0, D1[c], 2.0 * q1 * D0[c]) * frcp(fma(2.0, q1, q0)));
+        }
+#else
+        const double e0 = eps + D0[c] * D0[c];
+        const double e1 = eps + D1[c] * D1[c];
+        const double q0 = e0 * e0;
+        const double q1 = e1 * e1;
+        if constexpr (RECON == RECON_WENO2) {
+          const double a0 = 0.5 / q0;
+          const double a1 = 0.5 / q1;
+          const double sm = a0 + a1;
+          dh[c] = 0.5 * ((a0 / sm) * D0[c] + (a1 / sm) * D1[c]);
+          dl[c] = dh[c];
+        } else {
+          constexpr double d0 = 1.0 / 3.0, d1 = 2.0 / 3.0;  // numerics.py:53
+          const double a0 = d0 / q0, a1 = d1 / q1;
+          const double sa = a0 + a1;
+          dh[c] = 0.5 * ((a0 / sa) * D0[c] + (a1 / sa) * D1[c]);
+          const double b0 = d0 / q1, b1 = d1 / q0;  // mirrored stencil
+          const double sb = b0 + b1;
+          dl[c] = 0.5 * ((b0 / sb) * D1[c] + (b1 / sb) * D0[c]);
+        }
+#endif
+      }
     }
 #pragma unroll
-    for (int c = 0; c < NC; ++c) weno_faces<RECON>(um[c], uc[c], up[c], eps, hi[c], lo[c]);
+    for (int c = 0; c < NC; ++c) {
+      hi[c] = uc[c] + dh[c];
+      lo[c] = uc[c] - dl[c];
+    }
   }
 }
 
@@ -321,8 +380,41 @@ __device__ __forceinline__ void interface_flux(const double* uL0, const double* 
   constexpr int NC = NComp<EQ, DIM>::value;
   if constexpr (EQ == EQ_EULER) {
     double uL[NC], uR[NC];
+    bool equal = true;
 #pragma unroll
-    for (int c = 0; c < NC; ++c) { uL[c] = uL0[c]; uR[c] = uR0[c]; }
+    for (int c = 0; c < NC; ++c) {
+      uL[c] = uL0[c];
+      uR[c] = uR0[c];
+      equal &= bit_eq(uL[c], uR[c]);
+    }
+    const unsigned am = __activemask();
+    if (!__any_sync(am, !equal)) {
+      // Whole warp on uniform states (the KH bands): F(u, u) = f(u) for
+      // HLLC (numerics.py:195-196) and Rusanov (0.5(f+f) - hs*(+0) == f), so
+      // only v and p of one state are needed -- no second state, no sqrt.
+#if FVB_FAST
+      const double r = frcp(uL[0]);
+      double msq = uL[1] * uL[1];
+#pragma unroll
+      for (int k = 1; k < DIM; ++k) msq = fma(uL[1 + k], uL[1 + k], msq);
+      const double p = P.gm1 * fma(-0.5 * msq, r, uL[1 + DIM]);
+      const double v = uL[1 + axis] * r;
+#else
+      const double p = euler_pressure<DIM>(uL, P);
+      const double v = uL[1 + axis] / uL[0];
+#endif
+      const bool ok = RECON == RECON_NONE || ((uL[0] > kFloor) & (p > kFloor));
+      if (__all_sync(am, ok)) {
+#if !FVB_FAST
+        if constexpr (FLUX == FLUX_HLLC) {  // the reference's degenerate-fan check still applies
+          const double c = sqrt(P.gamma * p / uL[0]);
+          if ((v + c) - (v - c) <= 0.0) errbits |= 1u;
+        }
+#endif
+        euler_flux<DIM>(uL, p, v, axis, F);
+        return;
+      }
+    }
     EState L = euler_state<DIM>(uL, axis, P);
     EState R = euler_state<DIM>(uR, axis, P);
     if constexpr (RECON != RECON_NONE) {

@@ -759,6 +759,10 @@ ring_kernel(const StageParams p) {
   double* lx = hx + (WENO ? NC * NT : 0);            // [NC][NT]
   double* gx = lx + (WENO ? NC * NT : 0);            // [NC][NT]
   double* nring = gx + NC * NT;                      // [3][NC][NT]: u^n rows for the RK combination
+  // march recurrence (high face H and flux G of the previous row) lives in
+  // shared memory, not registers: it is idle during the whole x sweep
+  double* hs = nring + 3 * NC * NT;                  // [NC][NT]
+  double* gs = hs + NC * NT;                         // [NC][NT]
   auto RG = [&](int slot, int c, int x) -> double& { return ring[(slot * NC + c) * W + x]; };
   auto NR = [&](int slot, int c) -> double& { return nring[(slot * NC + c) * NT + threadIdx.x]; };
 
@@ -781,7 +785,7 @@ ring_kernel(const StageParams p) {
   const int64_t hco = map_index(tx == 0 ? x0 - 2 : x0 + NT - 1, p.n[0], p.bc[0], p.g);
   const int hcol = tx == 0 ? 0 : NT + 1;
   // row offsets of rows ra-2 .. rb+PD+1, computed once per block
-  int64_t* rtab = reinterpret_cast<int64_t*>(nring + 3 * NC * NT);
+  int64_t* rtab = reinterpret_cast<int64_t*>(gs + NC * NT);
   for (int i = tx; i < p.H + kRingPD + 4; i += NT) rtab[i] = map_index(ra - 2 + i, p.n[1], p.bc[1], p.g) * p.sy;
   __syncthreads();
   auto roff = [&](int64_t r) -> int64_t { return rtab[r - (ra - 2)]; };
@@ -800,9 +804,6 @@ ring_kernel(const StageParams p) {
   // RK stage as a*u^n + b*(u^s + dt L) (solver.py:166-173); fast mode only
   const double rk_a = p.kind == 2 ? 0.5 : (p.kind == 3 ? 0.75 : (p.kind == 4 ? 1.0 / 3.0 : 0.0));
   const double rk_b = p.kind == 2 ? 0.5 : (p.kind == 3 ? 0.25 : (p.kind == 4 ? 2.0 / 3.0 : 1.0));
-  double H[NC], G[NC], R[NC];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) H[c] = G[c] = R[c] = 0.0;
 
   // prologue: rows ra-2 .. ra-1+PD (slot of row r = (r - ra + 2) % kRingRows)
   for (int k = 0; k < kRingPD + 2; ++k) {
@@ -854,17 +855,22 @@ ring_kernel(const StageParams p) {
       }
       weno_faces_nc<NC, RECON>(A, B, C, p.P.eps, hi, lo);
       if (r >= ra) {
-        double GC[NC];
+        double GC[NC], H[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) H[c] = hs[c * NT + tx];
         unsigned eb = 0;
         interface_flux<EQ, FLUX, DIM, RECON>(H, lo, A, B, 1, p.P, GC, eb);
         if (eb && cell) errb |= 2u;
         double v[NC];
+        const int tr = tx + 1 < NT ? tx + 1 : NT - 1;
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
+          // x residual of row r-1 straight from its fluxes (still in gx)
+          const double g0 = gx[c * NT + tx], g1 = gx[c * NT + tr], Gp = gs[c * NT + tx];
 #if FVB_FAST
-          const double Lc = fma(G[c] - GC[c], p.id[1], R[c]);
+          const double Lc = fma(Gp - GC[c], p.id[1], (g0 - g1) * p.id[0]);
 #else
-          const double Lc = R[c] - ddiv(GC[c] - G[c], p, 1);
+          const double Lc = (0.0 - ddiv(g1 - g0, p, 0)) - ddiv(GC[c] - Gp, p, 1);
 #endif
 #if FVB_FAST
           v[c] = p.kind == 0 ? Lc : fma(rk_a, unc[c], rk_b * fma(dt, Lc, A[c]));
@@ -879,10 +885,10 @@ ring_kernel(const StageParams p) {
           if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v, xf, r - 1, 0, smax);
         }
 #pragma unroll
-        for (int c = 0; c < NC; ++c) G[c] = GC[c];
+        for (int c = 0; c < NC; ++c) gs[c * NT + tx] = GC[c];
       }
 #pragma unroll
-      for (int c = 0; c < NC; ++c) H[c] = hi[c];
+      for (int c = 0; c < NC; ++c) hs[c * NT + tx] = hi[c];
     }
     if (r >= ra && r < rb) {  // in-plane (x) direction of row r, straight from the ring
       if constexpr (EQ == EQ_EULER) {
@@ -931,18 +937,8 @@ ring_kernel(const StageParams p) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) gx[c * NT + tx] = Gx[c];
       }
-      __syncthreads();
-      {
-        const int tr = tx + 1 < NT ? tx + 1 : NT - 1;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-#if FVB_FAST
-          R[c] = (gx[c * NT + tx] - gx[c * NT + tr]) * p.id[0];
-#else
-          R[c] = 0.0 - ddiv(gx[c * NT + tr] - gx[c * NT + tx], p, 0);
-#endif
-        }
-      }
+      // the x residual of this row is read from gx by the next iteration's
+      // finish, after that iteration's top barrier
     }
     sA = sB;
   }
@@ -959,7 +955,8 @@ ring_kernel(const StageParams p) {
 template <int EQ, int RECON, int NT>
 constexpr int ring_smem_bytes() {
   constexpr int NC = NComp<EQ, 2>::value;
-  return 8 * (kRingRows * NC * (NT + 2) + (RECON != RECON_NONE ? 2 : 0) * NC * NT + NC * NT + 3 * NC * NT);
+  return 8 * (kRingRows * NC * (NT + 2) + (RECON != RECON_NONE ? 2 : 0) * NC * NT + NC * NT + 3 * NC * NT +
+              2 * NC * NT);
 }
 
 // Standalone wave-speed pass: solver.py:128-136 (+ the initial is_physical
