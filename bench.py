@@ -123,12 +123,20 @@ def bench_ours(args, ws, rank, local):
     from paper_1912_07645_b200.initial import kelvin_helmholtz
     from paper_1912_07645_b200.solver import DeviceField, DeviceRun
 
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    dev_index = local % max(1, ndev)
+    torch.cuda.set_device(dev_index)
     dist = None
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one rank per GPU over NCCL; more ranks than GPUs (a smoke run on a
+        # small box) falls back to gloo for the barrier/timing reduce only --
+        # the replicas never exchange data
+        if ws <= ndev:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group("gloo")
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
 
@@ -170,7 +178,7 @@ def bench_ours(args, ws, rank, local):
     t_start = float(infos[0].t)
     torch.cuda.synchronize()
     evs = []
-    with Clocks(local) as clk:
+    with Clocks(dev_index) as clk:
         # sustained load so the clock sampler sees the part under this kernel
         tic = time.perf_counter()
         while time.perf_counter() - tic < args.sustain:
@@ -197,7 +205,8 @@ def bench_ours(args, ws, rank, local):
     if infos[0].err:
         raise RuntimeError(f"bench run failed: err {infos[0].err}/{infos[0].errsub}")
     if dist:
-        tt = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
+        on_gpu = dist.get_backend() == "nccl"
+        tt = torch.tensor([t_ms], device="cuda" if on_gpu else "cpu", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
     ms_per_step = t_ms / args.steps
