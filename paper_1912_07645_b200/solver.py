@@ -166,11 +166,16 @@ class DeviceField:
         N._require_cuda()  # no CPU fallback: fail loudly without a GPU
         src = torch.from_numpy(np.ascontiguousarray(field.data, dtype=np.float64))
         pinned = src.is_pinned()
-        if pin and not pinned:
-            src = src.pin_memory()
-            pinned = True
+        if not pinned:  # stage pageable input through a reused pinned buffer
+            key = ("h2d", tuple(src.shape))
+            stage = _STAGING.get(key)
+            if stage is None:
+                stage = torch.empty(tuple(src.shape), dtype=torch.float64, pin_memory=True)
+                _STAGING[key] = stage
+            stage.copy_(src)  # multi-threaded host copy
+            src = stage
         dev = torch.empty(src.shape, dtype=torch.float64, device=device or "cuda")
-        dev.copy_(src, non_blocking=pinned)
+        dev.copy_(src, non_blocking=not (src is _STAGING.get(("h2d", tuple(src.shape)))))
         return cls(field.grid, field.ncomp, dev)
 
     @property
@@ -216,7 +221,9 @@ def _d2h(t):
         buf = torch.empty(tuple(t.shape), dtype=torch.float64, pin_memory=True)
         _STAGING[key] = buf
     buf.copy_(t)
-    return buf.numpy().copy()
+    out = np.empty(tuple(t.shape))
+    torch.from_numpy(out).copy_(buf)  # multi-threaded host copy out of the staging buffer
+    return out
 
 
 def pinned_field(field):

@@ -23,3 +23,14 @@ for _ in range(20):
     out, _ = P.run_simulation(init, cfg, max_steps=10, arith="fast")
 torch.cuda.synchronize()
 print(sys.argv[1:], f"{(time.perf_counter() - a) / 20 * 1e3:.2f} ms per call")
+import numpy as np
+
+pageable = P.Field(grid, 4, np.array(init.data))
+for _ in range(2):
+    P.run_simulation(pageable, cfg, max_steps=10, arith="fast")
+torch.cuda.synchronize()
+a = time.perf_counter()
+for _ in range(20):
+    out, _ = P.run_simulation(pageable, cfg, max_steps=10, arith="fast")
+torch.cuda.synchronize()
+print("pageable input", f"{(time.perf_counter() - a) / 20 * 1e3:.2f} ms per call")
