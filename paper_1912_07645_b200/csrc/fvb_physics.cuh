@@ -226,6 +226,34 @@ __device__ __forceinline__ void weno_faces_nc(const double* um, const double* uc
         D0[c] = uc[c] - um[c];
         D1[c] = up[c] - uc[c];
       }
+#if FVB_FAST
+      if constexpr (RECON == RECON_WENO2 && NC > 1) {
+        // one reciprocal for all components: 1/den_c = (prod_{k!=c} den_k) / prod_k den_k
+        // (den_c = q0 + q1 >= 2 eps^2, so the product stays in range)
+        double den[NC], T[NC], pre[NC + 1], suf[NC + 1];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const double e0 = fma(D0[c], D0[c], eps);
+          const double e1 = fma(D1[c], D1[c], eps);
+          const double q0 = e0 * e0;
+          const double q1 = e1 * e1;
+          den[c] = q0 + q1;
+          T[c] = fma(q1, D0[c], q0 * D1[c]);
+        }
+        pre[0] = 1.0;
+        suf[NC] = 1.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) pre[c + 1] = pre[c] * den[c];
+#pragma unroll
+        for (int c = NC - 1; c >= 0; --c) suf[c] = suf[c + 1] * den[c];
+        const double inv = 0.5 * frcp(pre[NC]);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          dh[c] = ((inv * pre[c]) * suf[c + 1]) * T[c];
+          dl[c] = dh[c];
+        }
+      } else
+#endif
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
 #if FVB_FAST
