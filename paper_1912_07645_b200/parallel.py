@@ -30,8 +30,8 @@ import numpy as np
 
 from . import _native as N
 from . import errors as E
-from .grid import BoundaryKind, Field, GridSpec, make_field
-from .solver import (DeviceField, DeviceRun, TYPES, _raise_run_error, _v, check_scheme, make_layout, make_scheme)
+from .grid import Field, GridSpec, make_field
+from .solver import DeviceField, DeviceRun, TYPES, _raise_run_error, _v, check_scheme, make_layout
 
 _RECV_TIMEOUT = 60.0
 
@@ -204,11 +204,8 @@ def exchange_halos(field, rank: int, topo: RankTopology, transport: Transport, b
     packed/unpacked on the GPU (fvb_halo_pack/unpack)."""
     import torch
 
-    from .solver import fill_boundary_device
-
     dev, was_dev = (field, True) if isinstance(field, DeviceField) else (DeviceField.from_host(field), False)
     grid = dev.grid
-    g = grid.ghost_width
     ctx = N.context()
     s = _desc(grid, dev.ncomp)
     L = make_layout(grid, dev.ncomp)
@@ -216,8 +213,7 @@ def exchange_halos(field, rank: int, topo: RankTopology, transport: Transport, b
     for axis in range(grid.dim):
         periodic = _v(bc[axis]) == "periodic"
         nb = {side: topo.neighbor(rank, axis, side, periodic) for side in (0, 1)}
-        if nb[0] == rank and nb[1] == rank:
-            kinds = [BoundaryKind.PERIODIC if j == axis else BoundaryKind.OUTFLOW for j in range(grid.dim)]
+        if nb[0] == rank and nb[1] == rank:  # single rank along a periodic axis: plain wrap
             _fill_one_axis(dev, axis, "periodic")
             continue
         count = int(ctx.lib.fvb_halo_count(N.C.byref(s), axis))
@@ -254,9 +250,7 @@ def _fill_one_axis(dev, axis, kind):
 
 def _fill_one_side(dev, axis, side):
     """_fill_outflow_side (parallel.py:189-198): copy the nearest interior
-    layer into the ghost slab of one side (pack it, unpack it g times)."""
-    import torch
-
+    layer into the ghost slab of one side (a broadcast device copy)."""
     grid = dev.grid
     g = grid.ghost_width
     idx = [slice(None)] * dev.data.dim()

@@ -27,7 +27,7 @@ import numpy as np
 
 from . import _native as N
 from . import errors as E
-from .solver import DeviceField, DeviceRun, _raise_run_error, _v, check_scheme, make_layout, make_scheme
+from .solver import DeviceField, DeviceRun, _raise_run_error, check_scheme, make_layout, make_scheme
 
 MC = "mc"
 QMC = "qmc"
@@ -133,8 +133,6 @@ class FieldMoments:
 
     def update(self, field) -> None:
         """FieldMoments.update (uq.py:174-175) for one field."""
-        from .solver import make_scheme as _ms  # noqa: F401
-
         dev = field if isinstance(field, DeviceField) else DeviceField.from_host(field)
         ctx = N.context()
         s = _descriptor(dev.grid, dev.ncomp)
