@@ -43,6 +43,7 @@ def install_into(pkg) -> dict:
         bind(m, "run_parallel", _par.run_parallel)
     for m in (mods["uq"], mods["cli"]):
         bind(m, "run_mc", _uq.run_mc)
+        bind(m, "run_mlmc", _uq.run_mlmc)
     # result / error classes of the reference
     _sol.TYPES["TimeStepRecord"] = mods["solver"].TimeStepRecord
     _sol.TYPES["Field"] = mods["grid"].Field

@@ -50,6 +50,37 @@ class SamplePlan:
             raise E.ConfigError(f"stochastic_dim must be >= 1, got {self.stochastic_dim}")
 
 
+@dataclass(frozen=True)
+class MlmcPlan:
+    """Level grids coarsest to finest; every axis equal or doubled per level
+    (uq.py:47-76)."""
+
+    grids: tuple
+    samples_per_level: tuple
+    method: str = MC
+    seed: int = 0
+    stochastic_dim: int = 1
+
+    def __post_init__(self):
+        if len(self.grids) != len(self.samples_per_level):
+            raise E.ConfigError("need one sample count per level")
+        if len(self.grids) < 1:
+            raise E.ConfigError("MLMC needs at least one level")
+        if any(m < 1 for m in self.samples_per_level):
+            raise E.ConfigError("per-level sample counts must be >= 1")
+        for lvl in range(1, len(self.grids)):
+            coarse, fine = self.grids[lvl - 1], self.grids[lvl]
+            same = all(f == c for f, c in zip(fine.cells, coarse.cells))
+            doubled = all(f == 2 * c for f, c in zip(fine.cells, coarse.cells))
+            if not (same or doubled):
+                raise E.ConfigError(f"level {lvl} cells {fine.cells} are neither equal to nor double the "
+                                    f"level {lvl - 1} cells {coarse.cells}")
+
+    @property
+    def levels(self) -> int:
+        return len(self.grids)
+
+
 def radical_inverse(index: int, base: int) -> float:
     """Van der Corput radical inverse (uq.py:79-87)."""
     inv, factor = 0.0, 1.0 / base
@@ -302,45 +333,7 @@ def run_mc(plan, grid, cfg, evaluate_init, functionals, workers: int = 1, *, bat
         world, rank = dist.get_world_size(group), dist.get_rank(group)
     lo, hi = shard_range(plan.samples, world, rank)
     slots = [_Slot(f, grid, ncomp) for f in functionals]
-    B = batch or default_batch(grid, ncomp)
-    ctx = N.context()
-    layout = make_layout(grid, ncomp)
-    desc = make_scheme(grid, cfg, arith)
-    like = None
-    k = lo
-    while k < hi:
-        ks = list(range(k, min(hi, k + B)))
-        inits = []
-        for j in ks:
-            vec = draw_sample(plan, j)
-            try:
-                f0 = evaluate_init(grid, vec)
-            except Exception as exc:
-                raise E.SimulationError(f"sample {j} failed: {exc}") from exc
-            like = like or f0
-            inits.append(np.asarray(f0.data, dtype=np.float64))
-        host = torch.from_numpy(np.stack(inits))
-        b0 = host.to("cuda")
-        bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
-        run = DeviceRun(grid, cfg, bufs, len(ks), N.MODE_T_END, None, arith, log=False, ctx=ctx)
-        while True:
-            infos, done = run.poll()
-            if all(done):
-                break
-            left = max(((cfg.t_end - i.t) / i.dt) if (i.dt > 0 and not d) else 1 for i, d in zip(infos, done))
-            run.steps(int(min(512, max(1, math.ceil(left) + 2))))
-        infos = run.end()
-        for j, info in zip(ks, infos):
-            if info.err:
-                try:
-                    _raise_run_error(info, grid, ncomp)
-                except E.ConslawError as exc:
-                    raise E.SimulationError(f"sample {j} failed: {exc}") from exc
-        for i, j in enumerate(ks):
-            buf = bufs[int(infos[i].steps) % 2] if cfg.rk_order == 1 else bufs[0]
-            for s in slots:
-                s.push(ctx, desc, layout, buf, i, grid, ncomp, like)
-        k = ks[-1] + 1
+    _ensemble(plan, 0, grid, cfg, evaluate_init, slots, lo, hi, batch, arith)
     if dist is not None and world > 1:
         _merge_ranks(slots, dist, group, world)
     return [s.result() for s in slots]
@@ -364,6 +357,127 @@ def gather_ordered(tensors, count: int, dist, group, world):
         dist.all_gather(parts, src, group=group)
         gathered.append([x.to(dev) for x in parts] if host else parts)
     return [(int(cnts[r].item()), [g[r] for g in gathered]) for r in range(world)]
+
+
+def _ensemble(plan, level, grid, cfg, evaluate_init, slots, lo, hi, batch=None, arith=None):
+    """Samples [lo, hi) of one level: batched device runs (one instance per
+    sample), each final field pushed into every slot in sample order."""
+    import torch
+
+    ncomp = cfg.model.ncomp
+    B = batch or default_batch(grid, ncomp)
+    ctx = N.context()
+    layout = make_layout(grid, ncomp)
+    desc = make_scheme(grid, cfg, arith)
+    mlmc = hasattr(plan, "samples_per_level")
+    like = None
+    k = lo
+    while k < hi:
+        ks = list(range(k, min(hi, k + B)))
+        inits = []
+        for j in ks:
+            vec = draw_sample(plan, j, level)
+            try:
+                f0 = evaluate_init(grid, vec)
+            except Exception as exc:
+                where = f"level {level}, " if mlmc else ""
+                raise E.SimulationError(f"{where}sample {j} failed: {exc}") from exc
+            like = like or f0
+            inits.append(np.asarray(f0.data, dtype=np.float64))
+        b0 = torch.from_numpy(np.stack(inits)).to("cuda")
+        bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
+        run = DeviceRun(grid, cfg, bufs, len(ks), N.MODE_T_END, None, arith, log=False, ctx=ctx)
+        while True:
+            infos, done = run.poll()
+            if all(done):
+                break
+            left = max(((cfg.t_end - i.t) / i.dt) if (i.dt > 0 and not d) else 1 for i, d in zip(infos, done))
+            run.steps(int(min(512, max(1, math.ceil(left) + 2))))
+        infos = run.end()
+        for j, info in zip(ks, infos):
+            if info.err:
+                try:
+                    _raise_run_error(info, grid, ncomp)
+                except E.ConslawError as exc:
+                    where = f"level {level}, " if mlmc else ""
+                    raise E.SimulationError(f"{where}sample {j} failed: {exc}") from exc
+        for i, j in enumerate(ks):
+            buf = bufs[int(infos[i].steps) % 2] if cfg.rk_order == 1 else bufs[0]
+            for s in slots:
+                s.push(ctx, desc, layout, buf, i, grid, ncomp, like)
+        k = ks[-1] + 1
+
+
+@dataclass
+class MlmcMoments:
+    """Telescoped first/second moments on the finest grid (uq.py:325-331)."""
+
+    mean: np.ndarray
+    second_moment: np.ndarray
+    variance: np.ndarray
+
+
+def prolong(values, factor_per_axis):
+    """Piecewise-constant injection onto a finer grid (uq.py:334-345);
+    works on numpy arrays and on device tensors (component axis first, x last,
+    factors x-first)."""
+    dim = len(factor_per_axis)
+    out = values
+    for j in range(dim):
+        f = factor_per_axis[dim - 1 - j]
+        if f != 1:
+            out = np.repeat(out, f, axis=1 + j) if isinstance(out, np.ndarray) else out.repeat_interleave(f, dim=1 + j)
+    return out
+
+
+def _second_moment(fm):
+    """m2 / count + mean**2 (uq.py:155-158) on the device.  The count is a
+    full tensor: torch turns division by a host scalar into a multiplication
+    by its (rounded) reciprocal, which would not be bitwise."""
+    import torch
+
+    return fm._m2 / torch.full_like(fm._m2, float(fm.count)) + fm._mean * fm._mean
+
+
+def run_mlmc(plan, make_cfg, evaluate_init, workers: int = 1, *, batch: int | None = None,
+             arith: str | None = None):
+    """Multilevel estimate of the field mean and variance (uq.py:348-419):
+    every level's fine and coarse ensembles run as batched device runs with
+    on-GPU moment accumulation; the telescoping sums stay on the device."""
+    finest = plan.grids[-1]
+    mean_total = second_total = None
+    acc0 = None
+    for level in range(plan.levels):
+        grid_f = plan.grids[level]
+        cfg_f = make_cfg(grid_f)
+        slot = _Slot(FieldMoments(grid_f, cfg_f.model.ncomp), grid_f, cfg_f.model.ncomp)
+        _ensemble(plan, level, grid_f, cfg_f, evaluate_init, [slot], 0, plan.samples_per_level[level], batch, arith)
+        acc_f = slot.gpu
+        if level == 0:
+            acc0 = acc_f
+        factor_f = tuple(nf // nl for nf, nl in zip(finest.cells, grid_f.cells))
+        mean_l = prolong(acc_f._mean, factor_f)
+        second_l = prolong(_second_moment(acc_f), factor_f)
+        if level > 0:
+            grid_c = plan.grids[level - 1]
+            cfg_c = make_cfg(grid_c)
+            slot_c = _Slot(FieldMoments(grid_c, cfg_c.model.ncomp), grid_c, cfg_c.model.ncomp)
+            _ensemble(plan, level, grid_c, cfg_c, evaluate_init, [slot_c], 0, plan.samples_per_level[level], batch,
+                      arith)
+            fc = slot_c.gpu
+            factor_c = tuple(nf // nl for nf, nl in zip(finest.cells, grid_c.cells))
+            mean_l = mean_l - prolong(fc._mean, factor_c)
+            second_l = second_l - prolong(_second_moment(fc), factor_c)
+        if mean_total is None:
+            mean_total, second_total = mean_l, second_l
+        else:
+            mean_total = mean_total + mean_l
+            second_total = second_total + second_l
+    if plan.levels == 1:
+        variance = acc0.acc.variance(ddof=1)  # telescoping degenerates to single-level sampling
+    else:
+        variance = (second_total - mean_total * mean_total).cpu().numpy()
+    return MlmcMoments(mean_total.cpu().numpy(), second_total.cpu().numpy(), variance)
 
 
 def _merge_ranks(slots, dist, group, world):

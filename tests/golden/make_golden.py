@@ -34,7 +34,8 @@ from conslaw.iodsl.config import parse_config  # noqa: E402
 from conslaw.iodsl.expr import eval_init  # noqa: E402
 from conslaw.numerics import FluxKind, Reconstruction, ReconstructionKind  # noqa: E402
 from conslaw.solver import SchemeConfig, run_simulation, spatial_residual, wave_speed_maxima  # noqa: E402
-from conslaw.uq import FieldMoments, SamplePlan, StructureFunctionAccumulator, draw_sample, run_mc  # noqa: E402
+from conslaw.uq import (FieldMoments, MlmcPlan, SamplePlan, StructureFunctionAccumulator, draw_sample,  # noqa: E402
+                        run_mc, run_mlmc)
 
 OUT = Path(__file__).resolve().parent
 
@@ -393,6 +394,34 @@ def uq_case(name, text, samples, t_end, cells):
     return case
 
 
+def mlmc_cases():
+    """run_mlmc (uq.py:348-419): a 2-level KH2D hierarchy and the 1-level
+    degenerate case (bitwise equal to run_mc)."""
+    out = []
+    base = edit(edit(presets.KH2D, "scheme", "reconstruction", "weno2"), "scheme", "t_end", "0.01")
+    for name, cells, spl, method in (("kh2d_mlmc_2lvl", ("64 64", "128 128"), (4, 2), "mc"),
+                                     ("kh2d_mlmc_1lvl", ("128 128",), (3,), "mc"),
+                                     ("kh2d_mlmc_qmc_2lvl", ("64 64", "128 128"), (3, 2), "qmc")):
+        rcs = [parse_config(edit(base, "grid", "cells", c)) for c in cells]
+        grids = tuple(rc.grid for rc in rcs)
+        plan = MlmcPlan(grids, spl, method=method, seed=42, stochastic_dim=4)
+        rc0 = rcs[-1]
+
+        def make_cfg(grid, rc0=rc0):
+            return rc0.scheme
+
+        def ev(grid, vec, rc0=rc0):
+            return eval_init(rc0.initial_exprs, rc0.scheme.model, grid, vec, primitive=rc0.initial_primitive)
+
+        res = run_mlmc(plan, make_cfg, ev)
+        out.append({"name": name, "cells": [list(g.cells) for g in grids], "samples": list(spl), "method": method,
+                    "seed": 42, "stochastic_dim": 4, "scheme": scheme_dict(grids[-1], rc0.scheme),
+                    "mean_sha": sha(res.mean), "second_sha": sha(res.second_moment), "var_sha": sha(res.variance),
+                    "mean_sum": float(res.mean.sum()), "var_sum": float(res.variance.sum())})
+        print(name, out[-1]["mean_sha"], out[-1]["var_sha"])
+    return out
+
+
 def main():
     arrays: dict = {}
     gold: dict = {"numpy": np.__version__, "runs": [], "residuals": [], "errors": [], "uq": []}
@@ -452,6 +481,8 @@ def main():
     kq = edit(presets.KH2D, "uq", "method", "qmc")
     gold["uq"].append(uq_case("kh2d128_qmc8", kq, 8, 0.01, "128 128"))
     gold["uq"].append(uq_case("burgers128_qmc8", BURGERS_QMC, 8, 0.02, "128 128"))
+
+    gold["mlmc"] = mlmc_cases()
 
     mc = SamplePlan("mc", 8, 42, 4)
     qmc = SamplePlan("qmc", 8, 42, 4)
