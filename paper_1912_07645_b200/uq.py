@@ -247,6 +247,67 @@ class StructureFunctionAccumulator:
         return self.sums / self.samples
 
 
+class Histogram:
+    """Per-probe histogram of one component with under/overflow bins
+    (uq.py:181-228).  Only the probe values of each sample leave the GPU (a
+    gather of len(probe_cells) doubles); binning follows the reference
+    expression by expression."""
+
+    name = "histogram"
+
+    def __init__(self, probe_cells, component: int, lo: float, hi: float, bins: int = 64):
+        if hi <= lo:
+            raise E.ConfigError(f"histogram range [{lo}, {hi}) is empty")
+        if bins < 1:
+            raise E.ConfigError(f"histogram needs >= 1 bins, got {bins}")
+        self.probe_cells = tuple(tuple(int(i) for i in p) for p in probe_cells)
+        self.component = component
+        self.lo = float(lo)
+        self.hi = float(hi)
+        self.bins = int(bins)
+        self.counts = np.zeros((len(self.probe_cells), bins + 2), dtype=np.int64)
+        self.samples = 0
+
+    @property
+    def edges(self) -> np.ndarray:
+        return np.linspace(self.lo, self.hi, self.bins + 1)
+
+    def fresh(self):
+        return Histogram(self.probe_cells, self.component, self.lo, self.hi, self.bins)
+
+    def add_values(self, values) -> None:
+        width = (self.hi - self.lo) / self.bins
+        for p, v in enumerate(values):
+            v = float(v)
+            if v < self.lo:
+                self.counts[p, 0] += 1
+            elif v >= self.hi:
+                self.counts[p, -1] += 1
+            else:
+                self.counts[p, 1 + min(int((v - self.lo) / width), self.bins - 1)] += 1
+        self.samples += 1
+
+    def gather(self, data, grid):
+        """Probe values of one padded (ncomp, *data_shape) field (host or device)."""
+        g = grid.ghost_width
+        idx = [(self.component,) + tuple(g + i for i in reversed(cell)) for cell in self.probe_cells]
+        if isinstance(data, np.ndarray):
+            return [data[i] for i in idx]
+        import torch
+
+        cols = list(zip(*idx))
+        return data[tuple(torch.tensor(c, device=data.device) for c in cols)].cpu().numpy()
+
+    def update(self, field) -> None:
+        self.add_values(self.gather(field.data, field.grid))
+
+    def merge(self, other: "Histogram") -> None:
+        if other.counts.shape != self.counts.shape:
+            raise E.ConfigError("histogram shapes do not match")
+        self.counts += other.counts
+        self.samples += other.samples
+
+
 def _descriptor(grid, ncomp):
     s = N.Scheme()
     s.dim = grid.dim
@@ -275,13 +336,18 @@ class _Slot:
             self.gpu = FieldMoments(grid, ncomp)
         elif name == "structure_function":
             self.gpu = StructureFunctionAccumulator(proto.p, proto.max_offset, getattr(proto, "component", 0))
+        elif name == "histogram":
+            self.gpu = None
+            self.hist = Histogram(proto.probe_cells, proto.component, proto.lo, proto.hi, proto.bins)
         else:
-            self.gpu = None  # host functional (e.g. Histogram): fed host fields
+            self.gpu = None  # other host functionals: fed host fields
             self.host = proto.fresh()
 
     def push(self, ctx, scheme, layout, buf, inst, grid, ncomp, like):
         if self.gpu is not None:
             self.gpu.push_device(ctx, scheme, layout, buf, inst)
+        elif self.kind == "histogram":
+            self.hist.add_values(self.hist.gather(buf[inst], grid))
         else:
             one = DeviceField(grid, ncomp, buf[inst]).to_host(like)
             c = self.proto.fresh()
@@ -290,6 +356,12 @@ class _Slot:
 
     def result(self):
         """Return an object of the caller's functional type."""
+        if self.kind == "histogram":
+            if isinstance(self.proto, Histogram):
+                return self.hist
+            out = self.proto.fresh()
+            out.counts, out.samples = self.hist.counts, self.hist.samples
+            return out
         if self.gpu is None:
             return self.host
         if isinstance(self.proto, (FieldMoments, StructureFunctionAccumulator)):

@@ -394,6 +394,25 @@ def uq_case(name, text, samples, t_end, cells):
     return case
 
 
+def histogram_case():
+    """run_mc with a point-PDF Histogram functional (uq.py:181-228)."""
+    from conslaw.uq import Histogram
+
+    txt = edit(edit(edit(presets.KH2D, "grid", "cells", "128 128"), "scheme", "t_end", "0.01"),
+               "scheme", "reconstruction", "weno2")
+    rc = parse_config(txt)
+    plan = SamplePlan("mc", 8, 42, 4)
+
+    def ev(grid, vec):
+        return eval_init(rc.initial_exprs, rc.scheme.model, grid, vec, primitive=rc.initial_primitive)
+
+    probes = ((64, 32), (10, 96), (127, 0), (64, 64))
+    h = Histogram(probes, 0, 0.9, 2.1, 12)
+    (res,) = run_mc(plan, rc.grid, rc.scheme, ev, [h])
+    return {"probes": [list(p) for p in probes], "component": 0, "lo": 0.9, "hi": 2.1, "bins": 12,
+            "counts": res.counts.tolist(), "samples": res.samples, "scheme": scheme_dict(rc.grid, rc.scheme)}
+
+
 def mlmc_cases():
     """run_mlmc (uq.py:348-419): a 2-level KH2D hierarchy and the 1-level
     degenerate case (bitwise equal to run_mc)."""
@@ -483,6 +502,7 @@ def main():
     gold["uq"].append(uq_case("burgers128_qmc8", BURGERS_QMC, 8, 0.02, "128 128"))
 
     gold["mlmc"] = mlmc_cases()
+    gold["histogram"] = histogram_case()
 
     mc = SamplePlan("mc", 8, 42, 4)
     qmc = SamplePlan("qmc", 8, 42, 4)

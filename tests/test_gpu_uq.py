@@ -111,3 +111,15 @@ def test_run_mlmc_matches_reference(P, golden, name):
     assert O.sha16(res.mean) == case["mean_sha"]
     assert O.sha16(res.second_moment) == case["second_sha"]
     assert O.sha16(res.variance) == case["var_sha"]
+
+
+def test_histogram_functional_matches_reference(P, golden):
+    from paper_1912_07645_b200 import uq
+    from paper_1912_07645_b200.initial import kelvin_helmholtz
+
+    case = golden["histogram"]
+    grid, cfg = product_objects(case["scheme"])
+    h = uq.Histogram([tuple(p) for p in case["probes"]], case["component"], case["lo"], case["hi"], case["bins"])
+    (res,) = uq.run_mc(uq.SamplePlan("mc", 8, 42, 4), grid, cfg, kelvin_helmholtz, [h], arith="exact")
+    assert res.samples == case["samples"]
+    assert res.counts.tolist() == case["counts"]
