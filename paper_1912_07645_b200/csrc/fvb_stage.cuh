@@ -195,6 +195,15 @@ struct TileCtx {
   __device__ __forceinline__ double& GY(int c, int y, int x) const {
     return smem[nU + 2 * nFX + nGX + 2 * nFY + (c * NTY + y) * NT + x];
   }
+  // 3D: the z recurrence (high face H, flux G of the previous plane) lives
+  // in shared memory -- it is idle during the in-plane sweeps
+  static constexpr int nGY = PY ? NC * NTY * NT : 0;
+  __device__ __forceinline__ double& HS(int c) const {
+    return smem[nU + 2 * nFX + nGX + 2 * nFY + nGY + (c * NTY + ty) * NT + tx];
+  }
+  __device__ __forceinline__ double& GS(int c) const {
+    return smem[nU + 2 * nFX + nGX + 2 * nFY + nGY + NC * NTY * NT + (c * NTY + ty) * NT + tx];
+  }
 
   __device__ __forceinline__ int64_t roff(int64_t r) const {
     if constexpr (DIM == 2) return map_index(r, p.n[1], p.bc[1], p.g) * p.sy;
@@ -276,14 +285,16 @@ struct TileCtx {
       __syncthreads();
     }
     // interface fluxes: x interface tx sits between face cells tx-1 and tx
-    if (tx >= 1 && (!PY || (ty >= 1 && ty <= NTY - 2))) {
+    // (lane 0 computes an unused one: no divergence inside cell warps)
+    if (!PY || (ty >= 1 && ty <= NTY - 2)) {
+      const int tl = tx >= 1 ? tx - 1 : 0;
       double uL[NC], uR[NC], cl[NC], cr[NC], G[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         cl[c] = U(c, ty + OY, tx);
         cr[c] = U(c, ty + OY, tx + 1);
         if constexpr (WENO) {
-          uL[c] = HX(c, ty, tx - 1);
+          uL[c] = HX(c, ty, tl);
           uR[c] = LX(c, ty, tx);
         } else {
           uL[c] = cl[c];
@@ -292,12 +303,12 @@ struct TileCtx {
       }
       unsigned eb = 0;
       interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 0, p.P, G, eb);
-      if (eb && xf <= p.n[0] && (!PY || yf < p.n[1])) errb |= 1u;
+      if (eb && tx >= 1 && xf <= p.n[0] && (!PY || yf < p.n[1])) errb |= 1u;
 #pragma unroll
       for (int c = 0; c < NC; ++c) GX(c, ty, tx) = G[c];
     }
     if constexpr (PY) {
-      if (ty >= 1 && tx >= 1 && tx <= NT - 2) {
+      if (ty >= 1) {  // lanes 0 and NT-1 compute unused fluxes (no divergence)
         double uL[NC], uR[NC], cl[NC], cr[NC], G[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
@@ -313,7 +324,7 @@ struct TileCtx {
         }
         unsigned eb = 0;
         interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 1, p.P, G, eb);
-        if (eb && yf <= p.n[1] && xf < p.n[0]) errb |= 2u;
+        if (eb && tx >= 1 && tx <= NT - 2 && yf <= p.n[1] && xf < p.n[0]) errb |= 2u;
 #pragma unroll
         for (int c = 0; c < NC; ++c) GY(c, ty, tx) = G[c];
       }
@@ -356,27 +367,38 @@ struct TileCtx {
       double hi[NC], lo[NC];
       weno_faces_nc<NC, RECON>(A, B, C, p.P.eps, hi, lo);
       if (r >= ra) {
-        double GC[NC];
+        double GC[NC], Hc[NC], Gc[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          Hc[c] = PY ? HS(c) : H[c];
+          Gc[c] = PY ? GS(c) : G[c];
+        }
         unsigned eb = 0;
-        interface_flux<EQ, FLUX, DIM, RECON>(H, lo, A, B, MA, p.P, GC, eb);
+        interface_flux<EQ, FLUX, DIM, RECON>(Hc, lo, A, B, MA, p.P, GC, eb);
         if (eb && cell) errb |= 1u << MA;
         if (fin) {
           double Lc[NC];
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
 #if FVB_FAST
-            Lc[c] = fma(G[c] - GC[c], p.id[MA], R[c]);
+            Lc[c] = fma(Gc[c] - GC[c], p.id[MA], R[c]);
 #else
-            Lc[c] = R[c] - ddiv(GC[c] - G[c], p, MA);
+            Lc[c] = R[c] - ddiv(GC[c] - Gc[c], p, MA);
 #endif
           }
           finish(r - 1, A, unc, Lc);
         }
 #pragma unroll
-        for (int c = 0; c < NC; ++c) G[c] = GC[c];
+        for (int c = 0; c < NC; ++c) {
+          if constexpr (PY) GS(c) = GC[c];
+          else G[c] = GC[c];
+        }
       }
 #pragma unroll
-      for (int c = 0; c < NC; ++c) H[c] = hi[c];
+      for (int c = 0; c < NC; ++c) {
+        if constexpr (PY) HS(c) = hi[c];
+        else H[c] = hi[c];
+      }
     }
     if (r + 2 <= rb + 1) load_col(r + 2, A);  // A is dead: the row after next
     if (r >= ra && r < rb) inplane(r, B, R);
@@ -486,7 +508,7 @@ constexpr int stage_smem_bytes() {
   constexpr bool PY = DIM == 3;
   constexpr int SUY = PY ? NTY + 2 : 1;
   return 8 * (NC * SUY * (NT + 2) + (WENO ? 2 : 0) * NC * NTY * NT + NC * NTY * NT +
-              ((WENO && PY) ? 2 : 0) * NC * NTY * NT + (PY ? NC * NTY * NT : 0));
+              ((WENO && PY) ? 2 : 0) * NC * NTY * NT + (PY ? 3 * NC * NTY * NT : 0));
 }
 
 // ---------------------------------------------------------------------------

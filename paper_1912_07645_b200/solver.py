@@ -166,16 +166,14 @@ class DeviceField:
         N._require_cuda()  # no CPU fallback: fail loudly without a GPU
         src = torch.from_numpy(np.ascontiguousarray(field.data, dtype=np.float64))
         pinned = src.is_pinned()
-        if not pinned:  # stage pageable input through a reused pinned buffer
-            key = ("h2d", tuple(src.shape))
-            stage = _STAGING.get(key)
-            if stage is None:
-                stage = torch.empty(tuple(src.shape), dtype=torch.float64, pin_memory=True)
-                _STAGING[key] = stage
+        staged = not pinned
+        if staged:  # stage pageable input through a reused (per-thread) pinned buffer
+            stage = _staging(("h2d", tuple(src.shape)), tuple(src.shape))
             stage.copy_(src)  # multi-threaded host copy
             src = stage
         dev = torch.empty(src.shape, dtype=torch.float64, device=device or "cuda")
-        dev.copy_(src, non_blocking=not (src is _STAGING.get(("h2d", tuple(src.shape)))))
+        # the staging buffer is reused by the next call: copy synchronously
+        dev.copy_(src, non_blocking=not staged)
         return cls(field.grid, field.ncomp, dev)
 
     @property
@@ -203,7 +201,20 @@ class DeviceField:
         return DeviceField(self.grid, self.ncomp, self.data.clone())
 
 
-_STAGING: dict = {}
+_STAGING_TLS = __import__("threading").local()  # per-thread pinned staging buffers (ranks may be threads)
+
+
+def _staging(key, shape):
+    import torch
+
+    cache = getattr(_STAGING_TLS, "bufs", None)
+    if cache is None:
+        cache = _STAGING_TLS.bufs = {}
+    buf = cache.get(key)
+    if buf is None:
+        buf = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+        cache[key] = buf
+    return buf
 
 
 def _d2h(t):
@@ -215,11 +226,7 @@ def _d2h(t):
 
     if os.environ.get("FVB_D2H", "staged") != "staged":
         return t.cpu().numpy()
-    key = (tuple(t.shape), t.device.index)
-    buf = _STAGING.get(key)
-    if buf is None:
-        buf = torch.empty(tuple(t.shape), dtype=torch.float64, pin_memory=True)
-        _STAGING[key] = buf
+    buf = _staging(("d2h", tuple(t.shape), t.device.index), tuple(t.shape))
     buf.copy_(t)
     out = np.empty(tuple(t.shape))
     torch.from_numpy(out).copy_(buf)  # multi-threaded host copy out of the staging buffer
