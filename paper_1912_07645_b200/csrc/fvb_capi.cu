@@ -203,8 +203,23 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
     int64_t waves = 1;
     if (const char* e = getenv("FVB_BLOCKS_PER_SM")) per_sm = std::max(1, atoi(e));
     if (const char* e = getenv("FVB_WAVES")) waves = std::max(1, atoi(e));
-    const int64_t target = 148 * per_sm * waves;
-    int64_t want_chunks = (target + strips * ytiles * ninst - 1) / (strips * ytiles * ninst);
+    const int64_t slots = 148 * per_sm;
+    const int64_t base = strips * ytiles * ninst;
+    int64_t want_chunks = 1;
+    if (getenv("FVB_WAVES")) {
+      want_chunks = (slots * waves + base - 1) / base;
+    } else {
+      // march chunks: minimise (waves of resident blocks) x (rows per chunk +
+      // the 2 extra rows a chunk marches), i.e. wave quantisation against
+      // redundant halo rows (3D 256^3: 387 tiles on 296 slots -> 3 chunks)
+      int64_t best = -1;
+      for (int64_t c = 1; c <= std::max<int64_t>(1, nm / 4); ++c) {
+        const int64_t w = (base * c + slots - 1) / slots;
+        const int64_t cost = w * ((nm + c - 1) / c + 2);
+        if (best < 0 || cost < best) { best = cost; want_chunks = c; }
+        if (w > 64) break;
+      }
+    }
     want_chunks = std::max<int64_t>(1, std::min<int64_t>(want_chunks, nm));
     H = (nm + want_chunks - 1) / want_chunks;
     const char* env = getenv("FVB_MARCH_ROWS");
