@@ -462,112 +462,6 @@ __device__ __forceinline__ void interface_flux(const double* uL0, const double* 
   }
 }
 
-// Two independent 2D Euler + HLLC interfaces at once -- the x interface
-// (k = 0) and the y interface (k = 1) of one ring-march row.  Each interface
-// runs exactly the expression sequence of interface_flux / hllc above (so the
-// results are bitwise those of two separate calls in both arithmetic modes),
-// but as one straight-line region: the two dependent FP64 chains interleave,
-// which is what the latency-bound stage needs at 16 warps/SM.  Warp-uniform
-// interfaces take the single-interface path (its shortcut is cheaper).
-template <int RECON>
-__device__ __forceinline__ void interface_flux_pair2d(double (&uL)[2][4], double (&uR)[2][4],
-                                                      const double (&cL)[2][4], const double (&cR)[2][4],
-                                                      const Phys& P, double (&F)[2][4], unsigned (&eb)[2]) {
-  constexpr int DIM = 2, NC = 4;
-  const unsigned am = __activemask();
-  bool eq[2];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    eq[k] = true;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) eq[k] &= bit_eq(uL[k][c], uR[k][c]);
-  }
-  if (!__any_sync(am, !eq[0]) || !__any_sync(am, !eq[1])) {
-    interface_flux<EQ_EULER, FLUX_HLLC, DIM, RECON>(uL[0], uR[0], cL[0], cR[0], 0, P, F[0], eb[0]);
-    interface_flux<EQ_EULER, FLUX_HLLC, DIM, RECON>(uL[1], uR[1], cL[1], cR[1], 1, P, F[1], eb[1]);
-    return;
-  }
-  EState L[2], R[2];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    L[k] = euler_state<DIM>(uL[k], k, P);
-    R[k] = euler_state<DIM>(uR[k], k, P);
-  }
-  if constexpr (RECON != RECON_NONE) {  // positivity fallback (solver.py:116-125)
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const bool ok = (uL[k][0] > kFloor) & (L[k].p > kFloor) & (uR[k][0] > kFloor) & (R[k].p > kFloor);
-      if (!ok) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) { uL[k][c] = cL[k][c]; uR[k][c] = cR[k][c]; }
-        L[k] = euler_state<DIM>(uL[k], k, P);
-        R[k] = euler_state<DIM>(uR[k], k, P);
-      }
-    }
-  }
-  // hllc<DIM> body, both interfaces side by side (its whole-warp equal
-  // shortcut cannot fire here: both warps hold a differing lane)
-  double sL[2], sR[2], sM[2];
-  bool left[2], star[2];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const bool equal = (uL[k][0] == uR[k][0]) & (uL[k][1] == uR[k][1]) & (uL[k][2] == uR[k][2]) &
-                       (uL[k][3] == uR[k][3]);
-    sL[k] = np_min(L[k].v - L[k].c, R[k].v - R[k].c);
-    sR[k] = np_max(L[k].v + L[k].c, R[k].v + R[k].c);
-    if (sR[k] - sL[k] <= 0.0) eb[k] |= 1u;
-    const double den = L[k].rho * (sL[k] - L[k].v) - R[k].rho * (sR[k] - R[k].v);
-#if FVB_FAST
-    sM[k] = fdiv(fma(L[k].rho * L[k].v, sL[k] - L[k].v, R[k].p - L[k].p) - R[k].rho * R[k].v * (sR[k] - R[k].v),
-                 den);
-#else
-    sM[k] = (R[k].p - L[k].p + L[k].rho * L[k].v * (sL[k] - L[k].v) - R[k].rho * R[k].v * (sR[k] - R[k].v)) / den;
-#endif
-    left[k] = equal || (sL[k] >= 0.0) || (sM[k] >= 0.0);
-    star[k] = !equal && !(sL[k] >= 0.0) && ((sM[k] >= 0.0) || (sR[k] > 0.0));
-  }
-  double u[2][NC], rho[2], v[2], p[2], sK[2];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-#pragma unroll
-    for (int c = 0; c < NC; ++c) u[k][c] = left[k] ? uL[k][c] : uR[k][c];
-    rho[k] = left[k] ? L[k].rho : R[k].rho;
-    v[k] = left[k] ? L[k].v : R[k].v;
-    p[k] = left[k] ? L[k].p : R[k].p;
-    sK[k] = left[k] ? sL[k] : sR[k];
-    euler_flux<DIM>(u[k], p[k], v[k], k, F[k]);
-  }
-  if (!__any_sync(am, star[0] || star[1])) return;
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    double st[NC];
-#if FVB_FAST
-    const double rinv = left[k] ? L[k].rinv : R[k].rinv;
-    const double sKv = sK[k] - v[k];
-    const double rs = rho[k] * sKv;
-    const double fac = rs * frcp(sK[k] - sM[k]);
-    st[0] = fac;
-#pragma unroll
-    for (int j = 0; j < DIM; ++j) st[1 + j] = fac * (u[k][1 + j] * rinv);
-    st[1 + k] = fac * sM[k];
-    st[1 + DIM] = fac * fma(sM[k] - v[k], fma(p[k], frcp(rs), sM[k]), u[k][1 + DIM] * rinv);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) F[k][c] = star[k] ? fma(sK[k], st[c] - u[k][c], F[k][c]) : F[k][c];
-#else
-    const double fac = rho[k] * (sK[k] - v[k]) / (sK[k] - sM[k]);
-    st[0] = fac;
-#pragma unroll
-    for (int j = 0; j < DIM; ++j) {
-      if (j != k) st[1 + j] = fac * (u[k][1 + j] / rho[k]);
-    }
-    st[1 + k] = fac * sM[k];
-    st[1 + DIM] = fac * (u[k][1 + DIM] / rho[k] + (sM[k] - v[k]) * (sM[k] + p[k] / (rho[k] * (sK[k] - v[k]))));
-#pragma unroll
-    for (int c = 0; c < NC; ++c) F[k][c] = star[k] ? F[k][c] + sK[k] * (st[c] - u[k][c]) : F[k][c];
-#endif
-  }
-}
-
 // Max wave speed of one state along every axis (equations.py:113-125)
 template <int EQ, int DIM>
 __device__ __forceinline__ void wave_speeds(const double* u, const Phys& P, double* s) {

@@ -765,9 +765,6 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #ifndef FVB_RING_MINB
 #define FVB_RING_MINB (512 / FVB_RING_NT_FOR_MINB)
 #endif
-#ifndef FVB_RING_PAIR
-#define FVB_RING_PAIR 0
-#endif
 constexpr int kRingPD = 2;               // rows in flight ahead of the consumer
 constexpr int kRingRows = kRingPD + 3;   // ring slots
 
@@ -778,7 +775,6 @@ ring_kernel(const StageParams p) {
   constexpr int NC = NComp<EQ, DIM>::value;
   constexpr bool WENO = RECON != RECON_NONE;
   constexpr int W = NT + 2;
-  constexpr bool kPair = FVB_RING_PAIR && EQ == EQ_EULER && FLUX == FLUX_HLLC;
   extern __shared__ double smem[];
   double* ring = smem;                               // [kRingRows][NC][W]
   double* hx = ring + kRingRows * NC * W;            // [NC][NT]
@@ -870,97 +866,6 @@ ring_kernel(const StageParams p) {
       const int ns = (int)((r - 1 - ra) % 3);
 #pragma unroll
       for (int c = 0; c < NC; ++c) unc[c] = NR(ns, c);
-    }
-    if constexpr (kPair) {
-      if (r >= ra && r < rb) {  // interior row: both fluxes as one interleaved pair
-        double A[NC], B[NC], C[NC], hi[NC], lo[NC];
-        double uL2[2][4], uR2[2][4], cl2[2][4], cr2[2][4], F2[2][4];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          A[c] = RG(sA, c, tx + 1);
-          B[c] = RG(sB, c, tx + 1);
-          C[c] = RG(sC, c, tx + 1);
-        }
-        weno_faces_nc<NC, RECON>(A, B, C, p.P.eps, hi, lo);
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {  // high face of row r-1 out, of row r in (own column)
-          uL2[1][c] = hs[c * NT + tx];
-          hs[c * NT + tx] = hi[c];
-        }
-        if (p.check_input && cell && !euler_physical<DIM>(B, p.P))
-          atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | flat_cell<DIM>(p, xf, r, 0));
-        if constexpr (WENO) {
-          double um[NC], up[NC], xh[NC], xl[NC];
-#pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            um[c] = RG(sB, c, tx);
-            up[c] = RG(sB, c, tx + 2);
-          }
-          weno_faces_nc<NC, RECON>(um, B, up, p.P.eps, xh, xl);
-#pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            hx[c * NT + tx] = xh[c];
-            lx[c * NT + tx] = xl[c];
-          }
-        }
-        // x residual of row r-1 from its fluxes, before this row's overwrite them
-        double xr[NC];
-        {
-          const int tr = tx + 1 < NT ? tx + 1 : NT - 1;
-#pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            const double g0 = gx[c * NT + tx], g1 = gx[c * NT + tr];
-#if FVB_FAST
-            xr[c] = (g0 - g1) * p.id[0];
-#else
-            xr[c] = 0.0 - ddiv(g1 - g0, p, 0);
-#endif
-          }
-        }
-        __syncthreads();
-        const int tl = tx >= 1 ? tx - 1 : 0;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          cl2[0][c] = RG(sB, c, tx);
-          cr2[0][c] = B[c];
-          uL2[0][c] = WENO ? hx[c * NT + tl] : cl2[0][c];
-          uR2[0][c] = WENO ? lx[c * NT + tx] : B[c];
-          uR2[1][c] = lo[c];
-          cl2[1][c] = A[c];
-          cr2[1][c] = B[c];
-        }
-        unsigned eb2[2] = {0u, 0u};
-        interface_flux_pair2d<RECON>(uL2, uR2, cl2, cr2, p.P, F2, eb2);
-        if (eb2[0] && tx >= 1 && xf <= p.n[0]) errb |= 1u;
-        if (eb2[1] && cell) errb |= 2u;
-        if (r - 1 >= ra) {
-          double v[NC];
-#pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            const double Gp = gs[c * NT + tx];
-#if FVB_FAST
-            const double Lc = fma(Gp - F2[1][c], p.id[1], xr[c]);
-            v[c] = p.kind == 0 ? Lc : fma(rk_a, unc[c], rk_b * fma(dt, Lc, A[c]));
-#else
-            const double Lc = xr[c] - ddiv(F2[1][c] - Gp, p, 1);
-            v[c] = rk_combine(p.kind, unc[c], A[c], dt, Lc);
-#endif
-          }
-          if (fin) {
-            const int64_t o = co + roff(r - 1);
-#pragma unroll
-            for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
-            if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v, xf, r - 1, 0, smax);
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          gs[c * NT + tx] = F2[1][c];
-          gx[c * NT + tx] = F2[0][c];
-        }
-        sA = sB;
-        continue;
-      }
     }
     {  // march (y) direction: faces of row r, flux (r-1|r), finish row r-1
       double A[NC], B[NC], C[NC], hi[NC], lo[NC];
