@@ -181,7 +181,7 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
   p.variant = 2;
   if (kv && std::strcmp(kv, "strip") == 0) p.variant = 0;
   if (kv && std::strcmp(kv, "tile") == 0) p.variant = 1;
-  if (s.dim != 2 && p.variant == 2) p.variant = 1;
+  if (s.dim == 1 && p.variant == 2) p.variant = 1;
   if (s.arith == FVB_ARITH_FAST) fvb::fast::stage_block(s.dim, p.variant, nt, nty);
   else fvb::exact::stage_block(s.dim, p.variant, nt, nty);
   const int64_t strips = (p.n[0] + (nt - 2) - 1) / (nt - 2);

@@ -25,14 +25,37 @@ constexpr int kRingNT = FVB_RING_NT;
 void stage_block(int dim, int variant, int& nt, int& nty) {
   if (dim == 1 && variant == 2) variant = 1;
   if (dim == 2 && variant == 2) { nt = kRingNT; nty = 1; return; }
+  if (dim == 3 && variant == 2) { nt = kRing3NT; nty = kRing3NTY; return; }
   if (dim <= 2 && variant == 0) { nt = kStripCells * kStripWarps + 2; nty = 1; }
   else if (dim == 1) { nt = Blk<1>::NT; nty = 1; }
   else if (dim == 2) { nt = Blk<2>::NT; nty = 1; }
   else { nt = Blk<3>::NT; nty = Blk<3>::NTY; }
 }
 
+// opt a kernel into more than 48 KB of dynamic shared memory, once per device
+template <typename K>
+static void ensure_smem(K kern, int smem, unsigned& done_mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned bit = 1u << (dev & 31);
+  if (smem > 48 * 1024 && !(done_mask & bit)) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    done_mask |= bit;
+  }
+}
+
 template <int DIM, int EQ, int FLUX, int RECON, bool FIN>
 static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
+  if constexpr (DIM == 3) {
+    if (p.variant == 2) {
+      const int smem = ring3_smem_bytes<EQ>() + 8 * (p.H + 4);  // + plane-offset table
+      auto kern = ring3_kernel<EQ, FLUX, RECON, FIN>;
+      static unsigned done = 0;  // per instantiation
+      ensure_smem(kern, 227 * 1024, done);  // a cap: the plane table grows with H
+      kern<<<grid, dim3(kRing3NT, kRing3NTY), smem, s>>>(p);
+      return 0;
+    }
+  }
   if constexpr (DIM == 2) {
     if (p.variant == 2) {
       constexpr int NT = kRingNT;
@@ -48,11 +71,8 @@ static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
     constexpr int NT = Blk<DIM>::NT, NTY = Blk<DIM>::NTY;
     constexpr int smem = stage_smem_bytes<DIM, EQ, RECON, NT, NTY>();
     auto kern = stage_kernel<DIM, EQ, FLUX, RECON, NT, NTY, FIN>;
-    static bool attr_done = false;  // per instantiation
-    if (!attr_done) {
-      if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr_done = true;
-    }
+    static unsigned done = 0;  // per instantiation
+    ensure_smem(kern, smem, done);
     kern<<<grid, dim3(NT, NTY), smem, s>>>(p);
     return 0;
   }

@@ -982,6 +982,275 @@ constexpr int ring_smem_bytes() {
               2 * NC * NT);
 }
 
+// ---------------------------------------------------------------------------
+// 3D ring kernel (variant 2 in 3D): the 2D ring design on an in-plane tile.
+//
+// A block of 32 x 8 threads owns the 30 x 6 interior cells of its (x, y)
+// tile (thread <-> face cell, the outer ring of threads are the halo face
+// cells) and marches H planes along z.  Planes of the tile, WENO halos
+// included, stream into a 4-slot shared-memory ring by cp.async one plane
+// ahead, so no load ever stalls the math and the halo reads no longer sit
+// in front of a barrier.  Per plane: the z face / flux / finish of the
+// previous plane from the ring (own column, no barrier), then the in-plane
+// sweeps x and y one after the other through one face and one flux buffer
+// (fits two blocks per SM), the in-plane residual accumulating in
+// registers.  Row offsets come from a per-block table; the in-plane offsets
+// of every copy a thread issues are fixed for the whole march.
+// ---------------------------------------------------------------------------
+#ifndef FVB_RING3_MINB
+#define FVB_RING3_MINB 2
+#endif
+constexpr int kRing3NT = 32, kRing3NTY = 8, kRing3Slots = 4;
+
+template <int EQ, int FLUX, int RECON, bool FIN>
+__global__ void __launch_bounds__(kRing3NT * kRing3NTY, FVB_RING3_MINB)
+ring3_kernel(const StageParams p) {
+  constexpr int DIM = 3, NT = kRing3NT, NTY = kRing3NTY;
+  constexpr int NC = NComp<EQ, DIM>::value;
+  constexpr bool WENO = RECON != RECON_NONE;
+  constexpr int W = NT + 2, WY = NTY + 2, PL = WY * W, FB = NC * NTY * NT;
+  extern __shared__ double smem[];
+  double* ring = smem;                      // [slot][NC][WY][W]: planes, tile col j <-> x0-2+j, row i <-> y0-2+i
+  double* hf = ring + kRing3Slots * NC * PL;  // [NC][NTY][NT] faces (x sweep, then y sweep)
+  double* lf = hf + FB;
+  double* gf = lf + FB;                     // [NC][NTY][NT] fluxes (x sweep, then y sweep)
+  double* hs = gf + FB;                     // [NC][NTY][NT] z recurrence: high face of the previous plane
+  double* gs = hs + FB;                     //                             z flux below the previous plane
+  int64_t* rtab = reinterpret_cast<int64_t*>(gs + FB);
+  auto RG = [&](int slot, int c, int y, int x) -> double& { return ring[((slot * NC + c) * WY + y) * W + x]; };
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  auto FI = [&](int c, int y, int x) { return (c * NTY + y) * NT + x; };
+
+  const int inst = blockIdx.z / p.chunks;
+  const int chunk = blockIdx.z % p.chunks;
+  FvbState* st = p.st + (p.shared_state ? 0 : inst);
+  if (*(volatile int*)&st->done) return;
+  const double dt = p.kind == 0 ? 0.0 : *(volatile double*)&st->dt;
+  const double* __restrict__ us = p.us + p.origin + inst * p.si;
+  const double* un = p.un + p.origin + inst * p.si;
+  double* out = p.out + p.origin + inst * p.si;
+  const int64_t x0 = (int64_t)blockIdx.x * (NT - 2);
+  const int64_t y0 = (int64_t)blockIdx.y * (NTY - 2);
+  const int64_t xf = x0 - 1 + tx, yf = y0 - 1 + ty;
+  const bool inrow = ty >= 1 && ty <= NTY - 2;  // warp-uniform: interior face rows
+  const bool cell = inrow && tx >= 1 && tx <= NT - 2 && xf < p.n[0] && yf < p.n[1];
+  const int64_t ra = p.row_lo + (int64_t)chunk * p.H;
+  const int64_t rb = min(ra + (int64_t)p.H, p.row_hi);
+  const int64_t mxf = map_index(xf, p.n[0], p.bc[0], p.g), myf = map_index(yf, p.n[1], p.bc[1], p.g) * p.sy;
+  const int64_t co = mxf + myf;
+  // halo copies: lanes 0 / NT-1 also copy tile columns 0 / W-1 of their row,
+  // warps 0 / NTY-1 also copy tile rows 0 / WY-1 of their column
+  const bool hx_t = WENO && (tx == 0 || tx == NT - 1);
+  const int64_t hxo = map_index(tx == 0 ? x0 - 2 : x0 + NT - 1, p.n[0], p.bc[0], p.g) + myf;
+  const int hxc = tx == 0 ? 0 : W - 1;
+  const bool hy_t = WENO && (ty == 0 || ty == NTY - 1);
+  const int64_t hyo = mxf + map_index(ty == 0 ? y0 - 2 : y0 + NTY - 1, p.n[1], p.bc[1], p.g) * p.sy;
+  const int hyr = ty == 0 ? 0 : WY - 1;
+  const int tid = ty * NT + tx;
+  for (int i = tid; i < p.H + 4; i += NT * NTY) rtab[i] = map_index(ra - 2 + i, p.n[2], p.bc[2], p.g) * p.sz;
+  __syncthreads();
+  auto roff = [&](int64_t r) -> int64_t { return rtab[r - (ra - 2)]; };
+  auto fetch = [&](int64_t r, int slot) {
+    const int64_t ro = roff(r);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, ty + 1, tx + 1), us + co + ro + c * p.sc);
+    if (hx_t) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, ty + 1, hxc), us + hxo + ro + c * p.sc);
+    }
+    if (hy_t) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, hyr, tx + 1), us + hyo + ro + c * p.sc);
+    }
+  };
+
+  unsigned errb = 0;
+  double smax[DIM] = {0.0, 0.0, 0.0};
+  double R[NC], unc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) R[c] = unc[c] = 0.0;
+
+  // prologue: planes ra-2, ra-1, ra (slot of plane r = (r - ra + 2) % 4)
+  for (int k = 0; k < 3; ++k) {
+    fetch(ra - 2 + k, k);
+    cp_async_commit();
+  }
+  int sA = 0;  // slot of plane r-1 at the top of the loop
+  for (int64_t r = ra - 1; r <= rb; ++r) {
+    const int sB = (sA + 1) & 3, sC = (sA + 2) & 3;
+    if (r == ra) __syncthreads();  // iteration ra-1 had no in-plane barrier
+    if (r + 2 <= rb + 1) fetch(r + 2, (sA + 3) & 3);  // into the slot of plane r-2
+    cp_async_commit();
+    cp_async_wait<1>();  // planes up to r+1 have landed (own copies)
+    __syncthreads();     // ... everybody's
+    if (inrow) {  // z: faces of plane r, flux (r-1|r), finish plane r-1 (own column)
+      double A[NC], B[NC], C[NC], hi[NC], lo[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        A[c] = RG(sA, c, ty + 1, tx + 1);
+        B[c] = RG(sB, c, ty + 1, tx + 1);
+        C[c] = RG(sC, c, ty + 1, tx + 1);
+      }
+      weno_faces_nc<NC, RECON>(A, B, C, p.P.eps, hi, lo);
+      if (r >= ra) {
+        double H[NC], GC[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) H[c] = hs[FI(c, ty, tx)];
+        unsigned eb = 0;
+        interface_flux<EQ, FLUX, DIM, RECON>(H, lo, A, B, 2, p.P, GC, eb);
+        if (eb && cell) errb |= 4u;
+        if (r - 1 >= ra) {
+          double v[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const double Gp = gs[FI(c, ty, tx)];
+#if FVB_FAST
+            const double Lc = fma(Gp - GC[c], p.id[2], R[c]);
+#else
+            const double Lc = R[c] - ddiv(GC[c] - Gp, p, 2);
+#endif
+            v[c] = rk_combine(p.kind, unc[c], A[c], dt, Lc);
+          }
+          if (cell) {
+            const int64_t o = co + roff(r - 1);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
+            if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v, xf, yf, r - 1, smax);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) gs[FI(c, ty, tx)] = GC[c];
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) hs[FI(c, ty, tx)] = hi[c];
+    }
+    if (r >= ra && r < rb) {
+      // u^n of plane r for the next iteration's finish (latency covered by
+      // the in-plane sweeps)
+      if (p.kind >= 2 && cell) {
+        const int64_t o = co + roff(r);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) unc[c] = un[o + c * p.sc];
+      }
+      if constexpr (EQ == EQ_EULER) {  // stage-start interior check (solver.py:90-93)
+        if (p.check_input && cell) {
+          double B[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) B[c] = RG(sB, c, ty + 1, tx + 1);
+          if (!euler_physical<DIM>(B, p.P))
+            atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | flat_cell<DIM>(p, xf, yf, r));
+        }
+      }
+      // ---- x sweep (interior face rows) ----
+      if constexpr (WENO) {
+        if (inrow) {
+          double um[NC], uc[NC], up[NC], hi[NC], lo[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            um[c] = RG(sB, c, ty + 1, tx);
+            uc[c] = RG(sB, c, ty + 1, tx + 1);
+            up[c] = RG(sB, c, ty + 1, tx + 2);
+          }
+          weno_faces_nc<NC, RECON>(um, uc, up, p.P.eps, hi, lo);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            hf[FI(c, ty, tx)] = hi[c];
+            lf[FI(c, ty, tx)] = lo[c];
+          }
+        }
+        __syncthreads();
+      }
+      if (inrow) {  // x interface tx sits between face cells tx-1 and tx (lane 0's is unused)
+        const int tl = tx >= 1 ? tx - 1 : 0;
+        double uL[NC], uR[NC], cl[NC], cr[NC], G[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          cl[c] = RG(sB, c, ty + 1, tx);
+          cr[c] = RG(sB, c, ty + 1, tx + 1);
+          uL[c] = WENO ? hf[FI(c, ty, tl)] : cl[c];
+          uR[c] = WENO ? lf[FI(c, ty, tx)] : cr[c];
+        }
+        unsigned eb = 0;
+        interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 0, p.P, G, eb);
+        if (eb && tx >= 1 && xf <= p.n[0] && yf < p.n[1]) errb |= 1u;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) gf[FI(c, ty, tx)] = G[c];
+      }
+      __syncthreads();
+      if (inrow) {
+        const int tr = tx + 1 < NT ? tx + 1 : NT - 1;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+#if FVB_FAST
+          R[c] = (gf[FI(c, ty, tx)] - gf[FI(c, ty, tr)]) * p.id[0];
+#else
+          R[c] = 0.0 - ddiv(gf[FI(c, ty, tr)] - gf[FI(c, ty, tx)], p, 0);
+#endif
+        }
+      }
+      // ---- y sweep (all face rows) ----
+      if constexpr (WENO) {
+        double um[NC], uc[NC], up[NC], hi[NC], lo[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          um[c] = RG(sB, c, ty, tx + 1);
+          uc[c] = RG(sB, c, ty + 1, tx + 1);
+          up[c] = RG(sB, c, ty + 2, tx + 1);
+        }
+        weno_faces_nc<NC, RECON>(um, uc, up, p.P.eps, hi, lo);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          hf[FI(c, ty, tx)] = hi[c];
+          lf[FI(c, ty, tx)] = lo[c];
+        }
+      }
+      __syncthreads();  // y faces visible; every x residual read of gf done
+      if (ty >= 1) {  // y interface ty sits between face rows ty-1 and ty
+        double uL[NC], uR[NC], cl[NC], cr[NC], G[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          cl[c] = RG(sB, c, ty, tx + 1);
+          cr[c] = RG(sB, c, ty + 1, tx + 1);
+          uL[c] = WENO ? hf[FI(c, ty - 1, tx)] : cl[c];
+          uR[c] = WENO ? lf[FI(c, ty, tx)] : cr[c];
+        }
+        unsigned eb = 0;
+        interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 1, p.P, G, eb);
+        if (eb && tx >= 1 && tx <= NT - 2 && yf <= p.n[1] && xf < p.n[0]) errb |= 2u;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) gf[FI(c, ty, tx)] = G[c];
+      }
+      __syncthreads();
+      if (inrow) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+#if FVB_FAST
+          R[c] = fma(gf[FI(c, ty, tx)] - gf[FI(c, ty + 1, tx)], p.id[1], R[c]);
+#else
+          R[c] = R[c] - ddiv(gf[FI(c, ty + 1, tx)] - gf[FI(c, ty, tx)], p, 1);
+#endif
+        }
+      }
+      // gf / hf / lf are rewritten only after the next iteration's top barrier
+    }
+    sA = sB;
+  }
+  cp_async_wait<0>();
+  if (errb) {
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+      if (errb & (1u << a))
+        atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | ((long long)(1 + a) << 40));
+  }
+  if constexpr (FIN) block_epilogue<DIM>(p, st, inst, smax, true);
+}
+
+template <int EQ>
+constexpr int ring3_smem_bytes() {
+  constexpr int NC = NComp<EQ, 3>::value;
+  return 8 * (kRing3Slots * NC * (kRing3NTY + 2) * (kRing3NT + 2) + 5 * NC * kRing3NTY * kRing3NT);
+}
+
 // Standalone wave-speed pass: solver.py:128-136 (+ the initial is_physical
 // check of solver.py:211-212).  finalize = 1 also computes the first dt.
 template <int DIM, int EQ>
