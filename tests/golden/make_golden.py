@@ -206,6 +206,43 @@ vz = 0.15 * sin(2 * pi * (x + y))
 p = 1.0 + 0.1 * cos(2 * pi * (x - z))
 """
 
+SCALAR_3D = """\
+[grid]
+cells = 14 12 10
+extent = 1 1.2 0.8
+[scheme]
+equation = {eq}
+{speed}flux = rusanov
+reconstruction = {recon}
+rk_order = {rk}
+cfl = 0.4
+t_end = 0.08
+boundary = {bc}
+[initial]
+variables = scalar
+u = 0.6 + 0.5 * sin(2 * pi * x) * cos(2 * pi * y) + 0.3 * sin(2 * pi * z) + (x < 0.4 ? 0.5 : 0)
+"""
+
+EULER_3D_TILES = """\
+[grid]
+cells = 40 14 12
+extent = 2 0.7 0.6
+[scheme]
+equation = euler
+flux = hllc
+reconstruction = weno2
+rk_order = 3
+t_end = 0.02
+boundary = periodic
+[initial]
+variables = primitive
+rho = 1.0 + 0.3 * sin(2 * pi * x) * sin(2 * pi * z / 0.6) + (y < 0.35 ? 0.5 : 0)
+vx = 0.3 * cos(2 * pi * y / 0.7)
+vy = -0.1 * cos(2 * pi * x)
+vz = 0.15 * sin(2 * pi * (x + y))
+p = 1.0 + 0.1 * cos(2 * pi * (x - z))
+"""
+
 
 def run_case(name, text, sample=0, max_steps=None, store=False, arrays=None, vec=None):
     rc = parse_config(text)
@@ -492,6 +529,16 @@ def main():
         nm = f"euler3d_{flux}_{recon}_{bc}"
         runs.append(run_case(nm, EULER_3D.format(flux=flux, recon=recon, rk=3, bc=bc),
                              store=True, arrays=arrays))
+
+    # 3D scalar laws and a multi-tile / multi-chunk 3D Euler domain (the 3D
+    # ring kernel's one-component instantiations, tile seams, chunk seams)
+    for eq, recon, rk, bc in (("burgers", "weno2", 3, "periodic"), ("burgers", "weno3", 2, "outflow"),
+                              ("burgers", "none", 1, "periodic"), ("advection", "weno3", 3, "periodic"),
+                              ("advection", "none", 2, "outflow")):
+        nm = f"{eq}3d_{recon}_rk{rk}_{bc}"
+        runs.append(run_case(nm, SCALAR_3D.format(
+            eq=eq, recon=recon, rk=rk, bc=bc, speed="advection_speed = 0.7 -0.4 0.5\n" if eq == "advection" else ""), store=True, arrays=arrays))
+    runs.append(run_case("euler3d_tiles_hllc_weno2", EULER_3D_TILES, store=True, arrays=arrays))
 
     gold["residuals"] = residual_cases(arrays)
     gold["errors"] = error_cases()

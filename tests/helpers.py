@@ -52,3 +52,15 @@ def product_objects(d: dict):
                          rk_order=d["rk"], cfl=d["cfl"], t_end=d["t_end"],
                          bc=tuple(P.BoundaryKind(b) for b in d["bcs"]))
     return grid, cfg
+
+
+def _golden_run_names():
+    import json
+    from pathlib import Path
+
+    path = Path(__file__).resolve().parent / "golden" / "golden.json"
+    return [r["name"] for r in json.loads(path.read_text())["runs"]]
+
+
+# test ids for the per-run parametrisations (one test per golden run)
+GOLDEN_RUN_NAMES = _golden_run_names()

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from oracle import fv_oracle as O
-from tests.helpers import oracle_scheme, product_objects, rel_l1, rel_l1_field
+from tests.helpers import GOLDEN_RUN_NAMES, oracle_scheme, product_objects, rel_l1, rel_l1_field
 
 pytestmark = pytest.mark.gpu
 
@@ -32,12 +32,9 @@ def _init_field(P, case, arrays, grid):
     return P.Field(grid, data.shape[0], data)
 
 
-@pytest.mark.parametrize("idx", range(47))
-def test_run_simulation_exact_bitwise(P, golden, golden_arrays, idx):
-    runs = golden["runs"]
-    if idx >= len(runs):
-        pytest.skip("no such case")
-    case = runs[idx]
+@pytest.mark.parametrize("name", GOLDEN_RUN_NAMES)
+def test_run_simulation_exact_bitwise(P, golden, golden_arrays, name):
+    case = next(r for r in golden["runs"] if r["name"] == name)
     grid, cfg = product_objects(case["scheme"])
     init = _init_field(P, case, golden_arrays, grid)
     assert O.sha16(init.interior) == case["init_sha"]
@@ -188,3 +185,20 @@ def test_fast_mode_divergence_growth(P, golden, golden_arrays, name):
         print(f"{name} steps={m:3d} rel_l1_field={e:.3e} per-component={['%.2e' % x for x in per]}")
     assert rows[0][1] <= 1e-13
     assert all(e <= TOL_FAST for _, e, _ in rows)
+
+
+@pytest.mark.parametrize("kernel,name", [
+    ("tile", "kh2d64_weno2_50"), ("tile", "euler2d_hllc_weno3_outflow"), ("tile", "advection2d_weno3_rk3"),
+    ("strip", "kh2d64_weno2_50"), ("strip", "euler2d_rusanov_weno2_outflow"), ("strip", "burgers1d_weno3_rk3_outflow"),
+    ("tile", "euler3d_tiles_hllc_weno2"), ("tile", "burgers3d_weno3_rk2_outflow"), ("tile", "kh3d16_weno2_5"),
+])
+def test_alternate_stage_kernels_bitwise(P, golden, golden_arrays, monkeypatch, kernel, name):
+    """The non-default stage kernels (FVB_KERNEL=tile / strip: register-window
+    tile and warp-strip variants) reproduce the reference bitwise too."""
+    monkeypatch.setenv("FVB_KERNEL", kernel)
+    case = next(r for r in golden["runs"] if r["name"] == name)
+    grid, cfg = product_objects(case["scheme"])
+    init = _init_field(P, case, golden_arrays, grid)
+    final, recs = P.run_simulation(init, cfg, max_steps=case["max_steps"], arith="exact")
+    assert len(recs) == case["steps"], name
+    assert O.sha16(final.interior) == case["final_sha"], (kernel, name)
