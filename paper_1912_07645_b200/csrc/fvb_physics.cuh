@@ -401,10 +401,12 @@ __device__ __forceinline__ void hllc(const double* uL, const double* uR, const E
 // WENO only): if either reconstructed state is unphysical, both become the
 // adjacent cell values cL, cR.  The physical check reuses the per-state
 // pressure the flux needs anyway (same expression -> exact mode bitwise).
-template <int EQ, int FLUX, int DIM, int RECON>
-__device__ __forceinline__ void interface_flux(const double* uL0, const double* uR0, const double* cL,
-                                               const double* cR, int axis, const Phys& P, double* F,
-                                               unsigned& errbits) {
+// `cells(cL, cR)` loads the two adjacent cell states; it is called only on
+// the (rare) fallback path, so callers that keep the cells in shared memory
+// pay no loads for them.
+template <int EQ, int FLUX, int DIM, int RECON, typename CellsFn>
+__device__ __forceinline__ void interface_flux_lazy(const double* uL0, const double* uR0, CellsFn cells, int axis,
+                                                    const Phys& P, double* F, unsigned& errbits) {
   constexpr int NC = NComp<EQ, DIM>::value;
   if constexpr (EQ == EQ_EULER) {
     double uL[NC], uR[NC];
@@ -448,8 +450,7 @@ __device__ __forceinline__ void interface_flux(const double* uL0, const double* 
     if constexpr (RECON != RECON_NONE) {
       const bool ok = (uL[0] > kFloor) & (L.p > kFloor) & (uR[0] > kFloor) & (R.p > kFloor);
       if (!ok) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) { uL[c] = cL[c]; uR[c] = cR[c]; }
+        cells(uL, uR);
         L = euler_state<DIM>(uL, axis, P);
         R = euler_state<DIM>(uR, axis, P);
       }
@@ -460,6 +461,20 @@ __device__ __forceinline__ void interface_flux(const double* uL0, const double* 
     EState dummy{};
     rusanov<EQ, DIM>(uL0, uR0, dummy, dummy, axis, P, F);
   }
+}
+
+template <int EQ, int FLUX, int DIM, int RECON>
+__device__ __forceinline__ void interface_flux(const double* uL0, const double* uR0, const double* cL,
+                                               const double* cR, int axis, const Phys& P, double* F,
+                                               unsigned& errbits) {
+  constexpr int NC = NComp<EQ, DIM>::value;
+  interface_flux_lazy<EQ, FLUX, DIM, RECON>(
+      uL0, uR0,
+      [&](double* a, double* b) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) { a[c] = cL[c]; b[c] = cR[c]; }
+      },
+      axis, P, F, errbits);
 }
 
 // Max wave speed of one state along every axis (equations.py:113-125)

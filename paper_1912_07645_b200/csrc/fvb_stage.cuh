@@ -288,42 +288,42 @@ struct TileCtx {
     // (lane 0 computes an unused one: no divergence inside cell warps)
     if (!PY || (ty >= 1 && ty <= NTY - 2)) {
       const int tl = tx >= 1 ? tx - 1 : 0;
-      double uL[NC], uR[NC], cl[NC], cr[NC], G[NC];
+      double uL[NC], uR[NC], G[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
-        cl[c] = U(c, ty + OY, tx);
-        cr[c] = U(c, ty + OY, tx + 1);
-        if constexpr (WENO) {
-          uL[c] = HX(c, ty, tl);
-          uR[c] = LX(c, ty, tx);
-        } else {
-          uL[c] = cl[c];
-          uR[c] = cr[c];
-        }
+        uL[c] = WENO ? HX(c, ty, tl) : U(c, ty + OY, tx);
+        uR[c] = WENO ? LX(c, ty, tx) : U(c, ty + OY, tx + 1);
       }
+      auto cells = [&](double* a, double* b) {  // fallback only: loaded on demand
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          a[c] = U(c, ty + OY, tx);
+          b[c] = U(c, ty + OY, tx + 1);
+        }
+      };
       unsigned eb = 0;
-      interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 0, p.P, G, eb);
+      interface_flux_lazy<EQ, FLUX, DIM, RECON>(uL, uR, cells, 0, p.P, G, eb);
       if (eb && tx >= 1 && xf <= p.n[0] && (!PY || yf < p.n[1])) errb |= 1u;
 #pragma unroll
       for (int c = 0; c < NC; ++c) GX(c, ty, tx) = G[c];
     }
     if constexpr (PY) {
       if (ty >= 1) {  // lanes 0 and NT-1 compute unused fluxes (no divergence)
-        double uL[NC], uR[NC], cl[NC], cr[NC], G[NC];
+        double uL[NC], uR[NC], G[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          cl[c] = U(c, ty, tx + 1);
-          cr[c] = U(c, ty + 1, tx + 1);
-          if constexpr (WENO) {
-            uL[c] = HY(c, ty - 1, tx);
-            uR[c] = LY(c, ty, tx);
-          } else {
-            uL[c] = cl[c];
-            uR[c] = cr[c];
-          }
+          uL[c] = WENO ? HY(c, ty - 1, tx) : U(c, ty, tx + 1);
+          uR[c] = WENO ? LY(c, ty, tx) : U(c, ty + 1, tx + 1);
         }
+        auto cells = [&](double* a, double* b) {  // fallback only: loaded on demand
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            a[c] = U(c, ty, tx + 1);
+            b[c] = U(c, ty + 1, tx + 1);
+          }
+        };
         unsigned eb = 0;
-        interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 1, p.P, G, eb);
+        interface_flux_lazy<EQ, FLUX, DIM, RECON>(uL, uR, cells, 1, p.P, G, eb);
         if (eb && tx >= 1 && tx <= NT - 2 && yf <= p.n[1] && xf < p.n[0]) errb |= 2u;
 #pragma unroll
         for (int c = 0; c < NC; ++c) GY(c, ty, tx) = G[c];
@@ -941,21 +941,21 @@ ring_kernel(const StageParams p) {
       if constexpr (!WENO) __syncthreads();  // every lane has read row r-1's gx
       {  // x interface tx sits between face cells tx-1 and tx (lane 0's is unused)
         const int tl = tx >= 1 ? tx - 1 : 0;
-        double uL[NC], uR[NC], cl[NC], cr[NC], Gx[NC];
+        double uL[NC], uR[NC], Gx[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          cl[c] = RG(sB, c, tx);
-          cr[c] = RG(sB, c, tx + 1);
-          if constexpr (WENO) {
-            uL[c] = hx[c * NT + tl];
-            uR[c] = lx[c * NT + tx];
-          } else {
-            uL[c] = cl[c];
-            uR[c] = cr[c];
-          }
+          uL[c] = WENO ? hx[c * NT + tl] : RG(sB, c, tx);
+          uR[c] = WENO ? lx[c * NT + tx] : RG(sB, c, tx + 1);
         }
+        auto cells = [&](double* a, double* b) {  // fallback only: loaded on demand
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            a[c] = RG(sB, c, tx);
+            b[c] = RG(sB, c, tx + 1);
+          }
+        };
         unsigned eb = 0;
-        interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 0, p.P, Gx, eb);
+        interface_flux_lazy<EQ, FLUX, DIM, RECON>(uL, uR, cells, 0, p.P, Gx, eb);
         if (eb && tx >= 1 && xf <= p.n[0]) errb |= 1u;
 #pragma unroll
         for (int c = 0; c < NC; ++c) gx[c * NT + tx] = Gx[c];
@@ -1162,16 +1162,21 @@ ring3_kernel(const StageParams p) {
       }
       if (inrow) {  // x interface tx sits between face cells tx-1 and tx (lane 0's is unused)
         const int tl = tx >= 1 ? tx - 1 : 0;
-        double uL[NC], uR[NC], cl[NC], cr[NC], G[NC];
+        double uL[NC], uR[NC], G[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          cl[c] = RG(sB, c, ty + 1, tx);
-          cr[c] = RG(sB, c, ty + 1, tx + 1);
-          uL[c] = WENO ? hf[FI(c, ty, tl)] : cl[c];
-          uR[c] = WENO ? lf[FI(c, ty, tx)] : cr[c];
+          uL[c] = WENO ? hf[FI(c, ty, tl)] : RG(sB, c, ty + 1, tx);
+          uR[c] = WENO ? lf[FI(c, ty, tx)] : RG(sB, c, ty + 1, tx + 1);
         }
+        auto cells = [&](double* a, double* b) {  // fallback only: loaded on demand
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            a[c] = RG(sB, c, ty + 1, tx);
+            b[c] = RG(sB, c, ty + 1, tx + 1);
+          }
+        };
         unsigned eb = 0;
-        interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 0, p.P, G, eb);
+        interface_flux_lazy<EQ, FLUX, DIM, RECON>(uL, uR, cells, 0, p.P, G, eb);
         if (eb && tx >= 1 && xf <= p.n[0] && yf < p.n[1]) errb |= 1u;
 #pragma unroll
         for (int c = 0; c < NC; ++c) gf[FI(c, ty, tx)] = G[c];
@@ -1206,16 +1211,21 @@ ring3_kernel(const StageParams p) {
       }
       __syncthreads();  // y faces visible; every x residual read of gf done
       if (ty >= 1) {  // y interface ty sits between face rows ty-1 and ty
-        double uL[NC], uR[NC], cl[NC], cr[NC], G[NC];
+        double uL[NC], uR[NC], G[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          cl[c] = RG(sB, c, ty, tx + 1);
-          cr[c] = RG(sB, c, ty + 1, tx + 1);
-          uL[c] = WENO ? hf[FI(c, ty - 1, tx)] : cl[c];
-          uR[c] = WENO ? lf[FI(c, ty, tx)] : cr[c];
+          uL[c] = WENO ? hf[FI(c, ty - 1, tx)] : RG(sB, c, ty, tx + 1);
+          uR[c] = WENO ? lf[FI(c, ty, tx)] : RG(sB, c, ty + 1, tx + 1);
         }
+        auto cells = [&](double* a, double* b) {  // fallback only: loaded on demand
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            a[c] = RG(sB, c, ty, tx + 1);
+            b[c] = RG(sB, c, ty + 1, tx + 1);
+          }
+        };
         unsigned eb = 0;
-        interface_flux<EQ, FLUX, DIM, RECON>(uL, uR, cl, cr, 1, p.P, G, eb);
+        interface_flux_lazy<EQ, FLUX, DIM, RECON>(uL, uR, cells, 1, p.P, G, eb);
         if (eb && tx >= 1 && tx <= NT - 2 && yf <= p.n[1] && xf < p.n[0]) errb |= 2u;
 #pragma unroll
         for (int c = 0; c < NC; ++c) gf[FI(c, ty, tx)] = G[c];
