@@ -25,11 +25,12 @@
 namespace fvb {
 
 // numpy.maximum / numpy.minimum: NaN-propagating (numerics.py:138,164-165).
-// The fast mode uses the single-instruction fmax/fmin: they differ only on
+// The fast mode uses a plain compare + select (one DSETP, two FSEL; fmax
+// costs DSETP.MAX plus a NaN fix-up and register moves): it differs only on
 // NaN inputs, i.e. on states whose run is already failing a check.
 #if FVB_FAST
-__device__ __forceinline__ double np_max(double a, double b) { return fmax(a, b); }
-__device__ __forceinline__ double np_min(double a, double b) { return fmin(a, b); }
+__device__ __forceinline__ double np_max(double a, double b) { return a > b ? a : b; }
+__device__ __forceinline__ double np_min(double a, double b) { return a < b ? a : b; }
 #else
 __device__ __forceinline__ double np_max(double a, double b) { return (a > b || a != a) ? a : b; }
 __device__ __forceinline__ double np_min(double a, double b) { return (a < b || a != a) ? a : b; }
@@ -372,17 +373,22 @@ __device__ __forceinline__ void hllc(const double* uL, const double* uR, const E
   // star state (numerics.py:173-181), evaluated for the selected side only
   double st[NC];
 #if FVB_FAST
+  // one reciprocal serves 1/(sK - sM) and 1/(sK - v); lanes without a star
+  // state get a = 1 (everything stays finite) and a zero weight sKs, so the
+  // update needs no per-component select
   const double rinv = left ? L.rinv : R.rinv;
   const double sKv = sK - v;
-  const double rs = rho * sKv;
-  const double fac = rs * frcp(sK - sM);
+  const double a = star ? sK - sM : 1.0;
+  const double sKs = star ? sK : 0.0;
+  const double r2 = frcp(a * sKv);
+  const double fac = rho * (sKv * (r2 * sKv));  // rho (sK - v) / (sK - sM)
   st[0] = fac;
 #pragma unroll
   for (int j = 0; j < DIM; ++j) st[1 + j] = fac * (u[1 + j] * rinv);
   st[1 + axis] = fac * sM;
-  st[1 + DIM] = fac * fma(sM - v, fma(p, frcp(rs), sM), u[1 + DIM] * rinv);
+  st[1 + DIM] = fac * fma(sM - v, fma(p * rinv, r2 * a, sM), u[1 + DIM] * rinv);
 #pragma unroll
-  for (int c = 0; c < NC; ++c) F[c] = star ? fma(sK, st[c] - u[c], F[c]) : F[c];
+  for (int c = 0; c < NC; ++c) F[c] = fma(sKs, st[c] - u[c], F[c]);
 #else
   const double fac = rho * (sK - v) / (sK - sM);
   st[0] = fac;
