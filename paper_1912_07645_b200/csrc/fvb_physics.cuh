@@ -44,14 +44,14 @@ __device__ __forceinline__ bool bit_eq(double a, double b) {
 }
 
 #if FVB_FAST
-// 1/x: MUFU seed + two Newton steps (full double precision for normal x)
+// 1/x: MUFU seed (relative error e0 ~ 1e-6) + one third-order step
+// r (1 + e + e^2), e = 1 - x r: error e0^3 ~ 1e-18, below half an ulp, in
+// three DFMA instead of the four of two Newton steps
 __device__ __forceinline__ double frcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
 }
 // a/b with one residual correction
 __device__ __forceinline__ double fdiv(double a, double b) {
