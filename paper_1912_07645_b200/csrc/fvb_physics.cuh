@@ -53,12 +53,8 @@ __device__ __forceinline__ double frcp(double x) {
   const double e = fma(-x, r, 1.0);
   return fma(r, fma(e, e, e), r);
 }
-// a/b with one residual correction
-__device__ __forceinline__ double fdiv(double a, double b) {
-  const double r = frcp(b);
-  const double q = a * r;
-  return fma(fma(-b, q, a), r, q);
-}
+// a/b: a times the (<= 1 ulp) reciprocal, <= 2 ulp
+__device__ __forceinline__ double fdiv(double a, double b) { return a * frcp(b); }
 // sqrt(x), x > 0: rsqrt seed (~1e-6) + one Newton step on 1/sqrt (~1e-12),
 // then one residual correction of s = x*y.  Measured on the B200
 // (tools/mufu_precision.cu): equal to the correctly rounded sqrt for 4M
@@ -241,16 +237,38 @@ __device__ __forceinline__ void weno_faces_nc(const double* um, const double* uc
           den[c] = q0 + q1;
           T[c] = fma(q1, D0[c], q0 * D1[c]);
         }
-        pre[0] = 1.0;
-        suf[NC] = 1.0;
+        double rden[NC];  // 0.5 / den_c
+        if constexpr (NC == 4) {  // product tree: 9 multiplies for the 4 cofactors
+          const double p01 = den[0] * den[1], p23 = den[2] * den[3];
+          const double inv = 0.5 * frcp(p01 * p23);
+          const double a = inv * p23, b = inv * p01;
+          rden[0] = a * den[1];
+          rden[1] = a * den[0];
+          rden[2] = b * den[3];
+          rden[3] = b * den[2];
+        } else if constexpr (NC == 5) {
+          const double p01 = den[0] * den[1], p23 = den[2] * den[3], p234 = p23 * den[4];
+          const double inv = 0.5 * frcp(p01 * p234);
+          const double a = inv * p234, b = inv * p01, b4 = b * den[4];
+          rden[0] = a * den[1];
+          rden[1] = a * den[0];
+          rden[2] = b4 * den[3];
+          rden[3] = b4 * den[2];
+          rden[4] = b * p23;
+        } else {
+          pre[0] = 1.0;
+          suf[NC] = 1.0;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) pre[c + 1] = pre[c] * den[c];
+          for (int c = 0; c < NC; ++c) pre[c + 1] = pre[c] * den[c];
 #pragma unroll
-        for (int c = NC - 1; c >= 0; --c) suf[c] = suf[c + 1] * den[c];
-        const double inv = 0.5 * frcp(pre[NC]);
+          for (int c = NC - 1; c >= 0; --c) suf[c] = suf[c + 1] * den[c];
+          const double inv = 0.5 * frcp(pre[NC]);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) rden[c] = (inv * pre[c]) * suf[c + 1];
+        }
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          dh[c] = ((inv * pre[c]) * suf[c + 1]) * T[c];
+          dh[c] = rden[c] * T[c];
           dl[c] = dh[c];
         }
       } else
