@@ -409,7 +409,9 @@ def main():
         "config": {"workload": workload, "arith": args.arith,
                    "parity": "exact: bitwise == reference; fast: rel L1 <= 1e-12 (tests/test_gpu_parity.py)",
                    "l2": "flushed (256 MiB write) before every timed step",
-                   "state": f"timed from simulated t = {res['t_start']:.3f} (KH roll-up developed)",
+                   "state": (f"timed from the saved state {args.state_file} (+ t = {res['t_start']:.3f})"
+                             if args.state_file else
+                             f"timed from simulated t = {res['t_start']:.3f} (KH roll-up developed)"),
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
         "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"],
         "clocks": res["clocks"], "gpu_launches": int(res["launches"]),
