@@ -143,10 +143,23 @@ def bench_ours(args, ws, rank, local):
     n = args.cells
     dim = 3 if args.config == "kh3d" else 2
     grid = P.GridSpec(dim, (n,) * dim, (0.0,) * dim, (1.0,) * dim, ghost_width=2)
-    cfg = P.SchemeConfig(P.EquationModel("euler", dim), P.FluxKind.HLLC,
-                         P.Reconstruction(P.ReconstructionKind.WENO2), rk_order=3, cfl=0.475, t_end=2.0)
-    ninst = args.samples if args.config == "mc" else 1
-    if args.config == "mc":
+    burgers = args.config == "bqmc"
+    if burgers:  # configs[4]: the Burgers QMC preset scheme (Rusanov, WENO2, RK3, CFL 0.475)
+        cfg = P.SchemeConfig(P.EquationModel("burgers", dim), P.FluxKind.RUSANOV,
+                             P.Reconstruction(P.ReconstructionKind.WENO2), rk_order=3, cfl=0.475, t_end=2.0)
+    else:
+        cfg = P.SchemeConfig(P.EquationModel("euler", dim), P.FluxKind.HLLC,
+                             P.Reconstruction(P.ReconstructionKind.WENO2), rk_order=3, cfl=0.475, t_end=2.0)
+    ninst = args.samples if args.config in ("mc", "bqmc") else 1
+    if burgers:
+        from paper_1912_07645_b200.initial import burgers_sines
+        from paper_1912_07645_b200.uq import SamplePlan, draw_sample
+
+        plan = SamplePlan("qmc", ninst, 42, 2)
+        inits = [burgers_sines(grid, draw_sample(plan, k)) for k in range(ninst)]
+        init = inits[0]
+        b0 = torch.from_numpy(np.stack([f.data for f in inits])).to("cuda")
+    elif args.config == "mc":
         from paper_1912_07645_b200.uq import SamplePlan, draw_sample
 
         plan = SamplePlan("mc", ninst, 42, 4)
@@ -164,7 +177,7 @@ def bench_ours(args, ws, rank, local):
     run = DeviceRun(grid, cfg, bufs, ninst, N.MODE_FIXED, 1 << 40, args.arith, log=False)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     cells = n ** dim * ninst
-    ncomp = dim + 2
+    ncomp = 1 if burgers else dim + 2
 
     run.steps(args.warmup)
     # advance to a developed state (KH roll-up under way) before timing, so
@@ -198,6 +211,27 @@ def bench_ours(args, ws, rank, local):
             evs.append((a, b))
         torch.cuda.synchronize()
     launches = run.ctx.launches() - l0 - 0
+    stats = None
+    if burgers:  # the on-GPU statistics of configs[4]: moments + structure functions of every sample
+        from paper_1912_07645_b200.solver import make_layout
+        from paper_1912_07645_b200.uq import FieldMoments, StructureFunctionAccumulator, _descriptor
+
+        mom, sf = FieldMoments(grid, 1), StructureFunctionAccumulator(2.0, 8)
+        sch, lay = _descriptor(grid, 1), make_layout(grid, 1)
+        buf = bufs[run.result_buffer(infos[0])]
+        mom.push_device(run.ctx, sch, lay, buf, 0)  # warm: accumulator / partials allocations
+        sf.push_device(run.ctx, sch, lay, buf, 0)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for k in range(ninst):
+            mom.push_device(run.ctx, sch, lay, buf, k)
+            sf.push_device(run.ctx, sch, lay, buf, k)
+        b.record(stream)
+        torch.cuda.synchronize()
+        stats = {"ms_per_sample": round(a.elapsed_time(b) / ninst, 4),
+                 "what": "FieldMoments + StructureFunctionAccumulator(p=2, H=8) push of one final sample field"}
     step_ms = [a.elapsed_time(b) for a, b in evs]
     t_ms = float(sum(step_ms))
     infos, done = run.poll()
@@ -215,7 +249,8 @@ def bench_ours(args, ws, rank, local):
     # roofline: the 3 fused stage launches of a step (the only kernels in it)
     bytes_step = cells * 8 * ncomp * (2 + 3 + 3)  # stage1: r us, w out; stages 2-3: r us, un, w out
     kname = {"kh2d": "ring_kernel<EULER,HLLC,WENO2>", "mc": "ring_kernel<EULER,HLLC,WENO2> (batched)",
-             "kh3d": "stage_kernel<3,EULER,HLLC,WENO2>"}[args.config]
+             "kh3d": "ring3_kernel<EULER,HLLC,WENO2>",
+             "bqmc": "ring_kernel<BURGERS,RUSANOV,WENO2> (batched)"}[args.config]
     peak, peak_src = _hbm_peak()
     achieved = bytes_step / (ms_per_step * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -256,7 +291,7 @@ def bench_ours(args, ws, rank, local):
         dist.barrier()
     return {
         "value": value, "ms_per_step": ms_per_step, "roofline": roofline, "e2e": e2e,
-        "launches": launches, "clocks": clk.summary(), "step_ms": step_ms, "t_start": t_start,
+        "launches": launches, "clocks": clk.summary(), "step_ms": step_ms, "t_start": t_start, "stats": stats,
     }
 
 
@@ -346,10 +381,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--arith", default=os.environ.get("FVB_BENCH_ARITH", "fast"), choices=["fast", "exact"])
     ap.add_argument("--cells", type=int, default=None, help="cells per axis (default 1024 kh2d, 512 mc, 256 kh3d)")
-    ap.add_argument("--config", default="kh2d", choices=["kh2d", "mc", "kh3d"],
+    ap.add_argument("--config", default="kh2d", choices=["kh2d", "mc", "kh3d", "bqmc"],
                     help="kh2d: BASELINE configs[1] (headline); mc: batched KH2D ensemble (configs[2] "
-                         "shape); kh3d: KH3D single domain (configs[3] shape)")
-    ap.add_argument("--samples", type=int, default=16, help="mc: samples per GPU batch")
+                         "shape); kh3d: KH3D single domain (configs[3] shape); bqmc: batched Burgers QMC "
+                         "ensemble + structure functions (configs[4] shape)")
+    ap.add_argument("--samples", type=int, default=None, help="mc / bqmc: samples per GPU batch (16 / 4)")
     ap.add_argument("--cpu-steps", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--e2e-reps", type=int, default=3)
@@ -359,7 +395,11 @@ def main():
     ap.add_argument("--state-file", default=None, help="start from a saved developed state (profiling)")
     args = ap.parse_args()
     if args.cells is None:
-        args.cells = {"kh2d": N_CELLS, "mc": 512, "kh3d": 256}[args.config]
+        args.cells = {"kh2d": N_CELLS, "mc": 512, "kh3d": 256, "bqmc": 2048}[args.config]
+    if args.samples is None:
+        args.samples = 4 if args.config == "bqmc" else 16
+    if args.config == "bqmc" and args.warm_time == 1.0:
+        args.warm_time = 0.01  # the preset runs to t = 0.02
     ws, rank, local = _dist()
     workload = {
         "kh2d": f"KH2D {args.cells}x{args.cells} Euler, WENO2 + HLLC, SSP-RK3, periodic, fp64 "
@@ -368,6 +408,8 @@ def main():
               "batched (one instance per sample; configs[2] shape); step = one RK3 step of every sample",
         "kh3d": f"KH3D {args.cells}^3 Euler, WENO2 + HLLC, SSP-RK3, periodic, fp64 (configs[3] shape, "
                 "single domain); step = one RK3 time step",
+        "bqmc": f"Burgers 2D QMC ensemble, {args.samples} samples/GPU x {args.cells}^2, WENO2 + Rusanov, SSP-RK3, "
+                "fp64, batched (configs[4] shape); step = one RK3 step of every sample",
     }[args.config]
     cores = os.cpu_count() or 1
 
@@ -405,14 +447,19 @@ def main():
         "metric": METRIC, "value": round(res["value"], 4), "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms_per_step"], 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (KH2D preset initial data, MC seed 42 sample 0)",
+        "data": {"kh2d": "synthetic (KH2D preset initial data, MC seed 42 sample 0)",
+                 "mc": "synthetic (KH2D preset initial data, MC seed 42 samples 0..n-1)",
+                 "kh3d": "synthetic (KH3D initial data, MC seed 42 sample 0)",
+                 "bqmc": "synthetic (Burgers QMC preset initial data, Halton samples 0..n-1)"}[args.config],
         "config": {"workload": workload, "arith": args.arith,
                    "parity": "exact: bitwise == reference; fast: rel L1 <= 1e-12 (tests/test_gpu_parity.py)",
                    "l2": "flushed (256 MiB write) before every timed step",
                    "state": (f"timed from the saved state {args.state_file} (+ t = {res['t_start']:.3f})"
                              if args.state_file else
-                             f"timed from simulated t = {res['t_start']:.3f} (KH roll-up developed)"),
+                             f"timed from simulated t = {res['t_start']:.3f}"
+                             + ("" if args.config == "bqmc" else " (KH roll-up developed)")),
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+        **({"uq_stats": res["stats"]} if res.get("stats") else {}),
         "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"],
         "clocks": res["clocks"], "gpu_launches": int(res["launches"]),
     }

@@ -5,6 +5,7 @@
 //   * structure-function sums (uq.py:231-273), deterministic two-pass reduce
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "../../include/fvb200.h"
@@ -119,29 +120,32 @@ __global__ void halo_kernel(Pad p, fvb_layout L, double* u, int ncomp, int axis,
 // merged by uq.py:135-148 (first merge copies).
 __global__ void moments_push_kernel(Pad p, fvb_layout L, const double* u, int ncomp, int inst, double* mean,
                                     double* m2, long long count) {
-  const int64_t ncell = p.n[0] * p.n[1] * p.n[2];
-  const int64_t total = ncell * ncomp;
+  // block-strided over (component, z, y) rows, threads over x: no per-element
+  // index division; the (mean, m2) arrays are dense (ncomp, z, y, x)
+  const int64_t nrow = p.n[1] * p.n[2];
   const double frac = 1.0 / (double)(count + 1);   // other.count / total (int / int)
   const double fc = (double)count;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i / ncell);
-    int64_t r = i % ncell;
-    const int64_t x = r % p.n[0];
-    r /= p.n[0];
-    const int64_t y = r % p.n[1];
-    const int64_t z = r / p.n[1];
-    const double v = u[L.origin + inst * L.si + c * L.sc + x + y * L.sy + z * L.sz];
-    const double d0 = v - 0.0;
-    const double om = 0.0 + d0 / 1.0;
-    const double om2 = 0.0 + d0 * (v - om);
-    if (count == 0) {
-      mean[i] = om;
-      m2[i] = om2;
-    } else {
-      const double mu = mean[i];
-      const double delta = om - mu;
-      mean[i] = mu + delta * frac;
-      m2[i] = (m2[i] + om2) + ((delta * delta) * fc) * frac;
+  for (int64_t row = blockIdx.x; row < nrow * ncomp; row += gridDim.x) {
+    const int c = (int)(row / nrow);
+    const int64_t yz = row - (int64_t)c * nrow;
+    const int64_t y = yz % p.n[1], z = yz / p.n[1];
+    const double* src = u + L.origin + inst * L.si + c * L.sc + y * L.sy + z * L.sz;
+    double* mrow = mean + row * p.n[0];
+    double* qrow = m2 + row * p.n[0];
+    for (int64_t x = threadIdx.x; x < p.n[0]; x += blockDim.x) {
+      const double v = src[x];
+      const double d0 = v - 0.0;
+      const double om = 0.0 + d0 / 1.0;
+      const double om2 = 0.0 + d0 * (v - om);
+      if (count == 0) {
+        mrow[x] = om;
+        qrow[x] = om2;
+      } else {
+        const double mu = mrow[x];
+        const double delta = om - mu;
+        mrow[x] = mu + delta * frac;
+        qrow[x] = (qrow[x] + om2) + ((delta * delta) * fc) * frac;
+      }
     }
   }
 }
@@ -169,29 +173,31 @@ constexpr int kSfThreads = 256;
 
 // Pass 1: per-block partial sums S[h][j] of |w(x + h e_j) - w(x)|^p, where
 // j is the NUMPY axis (0 = slowest), matching np.roll(w, -h, axis=j).
+// Blocks stride over the (z, y) rows, threads over x (no per-element index
+// division); the shifted reads hit L2 (the field is L2-resident).  Fixed
+// partition and reduction order: deterministic.
 __global__ void __launch_bounds__(kSfThreads) structure_pass1(Pad p, fvb_layout L, const double* u, int inst,
                                                               int comp, double pw, int H, double* partials) {
   __shared__ double red[kSfThreads / 32];
   const int dim = p.dim;
-  const int64_t ncell = p.n[0] * p.n[1] * p.n[2];
+  const int64_t nrow = p.n[1] * p.n[2];
   const double* w = u + L.origin + inst * L.si + comp * L.sc;
   for (int h = 0; h <= H; ++h) {
     for (int j = 0; j < dim; ++j) {
       const int k = dim - 1 - j;  // spatial axis of numpy axis j
+      const int64_t hk = h % p.n[k];
       double acc = 0.0;
-      for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncell;
-           i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t c3[3];
-        int64_t r = i;
-        c3[0] = r % p.n[0]; r /= p.n[0];
-        c3[1] = r % p.n[1];
-        c3[2] = r / p.n[1];
-        const int64_t o = c3[0] + c3[1] * L.sy + c3[2] * L.sz;
-        int64_t s3[3] = {c3[0], c3[1], c3[2]};
-        s3[k] = (c3[k] + h) % p.n[k];
-        const int64_t os = s3[0] + s3[1] * L.sy + s3[2] * L.sz;
-        const double d = fabs(w[os] - w[o]);
-        acc += pw == 2.0 ? d * d : (pw == 1.0 ? d : pow(d, pw));
+      for (int64_t row = blockIdx.x; row < nrow; row += gridDim.x) {
+        const int64_t y = row % p.n[1], z = row / p.n[1];
+        const int64_t o = y * L.sy + z * L.sz;
+        int64_t os = o;  // shifted row for k = 1, 2
+        if (k == 1) os = ((y + hk < p.n[1]) ? y + hk : y + hk - p.n[1]) * L.sy + z * L.sz;
+        if (k == 2) os = y * L.sy + ((z + hk < p.n[2]) ? z + hk : z + hk - p.n[2]) * L.sz;
+        for (int64_t x = threadIdx.x; x < p.n[0]; x += blockDim.x) {
+          const int64_t xs = k == 0 ? ((x + hk < p.n[0]) ? x + hk : x + hk - p.n[0]) : x;
+          const double d = fabs(w[os + xs] - w[o + x]);
+          acc += pw == 2.0 ? d * d : (pw == 1.0 ? d : pow(d, pw));
+        }
       }
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
       if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
@@ -346,8 +352,9 @@ int launch_halo_instances(const fvb_scheme& s, const fvb_layout& L, double* u, i
 int launch_moments_push(const fvb_scheme& s, const fvb_layout& L, const double* u, int inst, double* mean,
                         double* m2, int64_t count_before, cudaStream_t st) {
   const Pad p = make_pad(s);
-  const int64_t n = p.n[0] * p.n[1] * p.n[2] * s.ncomp;
-  moments_push_kernel<<<grid_for(n), 256, 0, st>>>(p, L, u, s.ncomp, inst, mean, m2, (long long)count_before);
+  const int64_t rows = p.n[1] * p.n[2] * s.ncomp;
+  const int blocks = (int)std::min<int64_t>(rows, 148 * 16);
+  moments_push_kernel<<<blocks, 256, 0, st>>>(p, L, u, s.ncomp, inst, mean, m2, (long long)count_before);
   return 0;
 }
 
@@ -359,7 +366,8 @@ int launch_moments_merge(double* ma, double* m2a, int64_t ca, const double* mb, 
 
 int structure_blocks(const fvb_scheme& s) {
   const Pad p = make_pad(s);
-  return grid_for(p.n[0] * p.n[1] * p.n[2]) > 148 * 4 ? 148 * 4 : grid_for(p.n[0] * p.n[1] * p.n[2]);
+  const int64_t rows = p.n[1] * p.n[2];
+  return (int)std::min<int64_t>(rows, 148 * 8);
 }
 
 int launch_structure(const fvb_scheme& s, const fvb_layout& L, const double* u, int inst, int comp, double pw,
