@@ -21,6 +21,7 @@ StructureFunctionAccumulator prototypes are accepted and returned filled.
 from __future__ import annotations
 
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -405,7 +406,7 @@ def run_mc(plan, grid, cfg, evaluate_init, functionals, workers: int = 1, *, bat
         world, rank = dist.get_world_size(group), dist.get_rank(group)
     lo, hi = shard_range(plan.samples, world, rank)
     slots = [_Slot(f, grid, ncomp) for f in functionals]
-    _ensemble(plan, 0, grid, cfg, evaluate_init, slots, lo, hi, batch, arith)
+    _ensemble(plan, 0, grid, cfg, evaluate_init, slots, lo, hi, batch, arith, workers)
     if dist is not None and world > 1:
         _merge_ranks(slots, dist, group, world)
     return [s.result() for s in slots]
@@ -431,9 +432,34 @@ def gather_ordered(tensors, count: int, dist, group, world):
     return [(int(cnts[r].item()), [g[r] for g in gathered]) for r in range(world)]
 
 
-def _ensemble(plan, level, grid, cfg, evaluate_init, slots, lo, hi, batch=None, arith=None):
+_PINNED: dict = {}
+_PINNED_LOCK = threading.Lock()
+
+
+def _pinned_stage(key):
+    """Persistent pinned host buffer for (owner thread, parity, shape)."""
+    import torch
+
+    with _PINNED_LOCK:
+        buf = _PINNED.get(key)
+        if buf is None:
+            buf = _PINNED[key] = torch.empty(key[2], dtype=torch.float64, pin_memory=True)
+        return buf
+
+
+def _ensemble(plan, level, grid, cfg, evaluate_init, slots, lo, hi, batch=None, arith=None, workers=1):
     """Samples [lo, hi) of one level: batched device runs (one instance per
-    sample), each final field pushed into every slot in sample order."""
+    sample), each final field pushed into every slot in sample order.
+
+    The host-side initial data of batch b+1 (the caller's ``evaluate_init``,
+    stacked into pinned memory) is prepared on helper threads while batch b
+    runs on the GPU -- ``workers`` of them evaluate samples concurrently, the
+    role the reference gives its thread pool (uq.py:302-322); a failing
+    sample raises at the same point, with the same message, as without the
+    overlap (the lowest failing sample of the batch, after batch b has been
+    pushed)."""
+    import concurrent.futures as cf
+
     import torch
 
     ncomp = cfg.model.ncomp
@@ -442,42 +468,64 @@ def _ensemble(plan, level, grid, cfg, evaluate_init, slots, lo, hi, batch=None, 
     layout = make_layout(grid, ncomp)
     desc = make_scheme(grid, cfg, arith)
     mlmc = hasattr(plan, "samples_per_level")
-    like = None
-    k = lo
-    while k < hi:
-        ks = list(range(k, min(hi, k + B)))
-        inits = []
-        for j in ks:
-            vec = draw_sample(plan, j, level)
-            try:
-                f0 = evaluate_init(grid, vec)
-            except Exception as exc:
-                where = f"level {level}, " if mlmc else ""
+    where = f"level {level}, " if mlmc else ""
+    batches = [list(range(k, min(hi, k + B))) for k in range(lo, hi, B)]
+
+    nw = max(1, int(workers or 1))
+    evals = cf.ThreadPoolExecutor(max_workers=nw) if nw > 1 else None
+
+    def one(j):
+        try:
+            return evaluate_init(grid, draw_sample(plan, j, level)), None
+        except Exception as exc:  # reported in sample order by prepare()
+            return None, exc
+
+    owner = threading.get_ident()
+
+    def prepare(ks, parity):
+        outs = list(evals.map(one, ks)) if evals else [one(j) for j in ks]
+        for j, (_, exc) in zip(ks, outs):
+            if exc is not None:
                 raise E.SimulationError(f"{where}sample {j} failed: {exc}") from exc
-            like = like or f0
-            inits.append(np.asarray(f0.data, dtype=np.float64))
-        b0 = torch.from_numpy(np.stack(inits)).to("cuda")
-        bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
-        run = DeviceRun(grid, cfg, bufs, len(ks), N.MODE_T_END, None, arith, log=False, ctx=ctx)
-        while True:
-            infos, done = run.poll()
-            if all(done):
-                break
-            left = max(((cfg.t_end - i.t) / i.dt) if (i.dt > 0 and not d) else 1 for i, d in zip(infos, done))
-            run.steps(int(min(512, max(1, math.ceil(left) + 2))))
-        infos = run.end()
-        for j, info in zip(ks, infos):
-            if info.err:
-                try:
-                    _raise_run_error(info, grid, ncomp)
-                except E.ConslawError as exc:
-                    where = f"level {level}, " if mlmc else ""
-                    raise E.SimulationError(f"{where}sample {j} failed: {exc}") from exc
-        for i, j in enumerate(ks):
-            buf = bufs[int(infos[i].steps) % 2] if cfg.rk_order == 1 else bufs[0]
-            for s in slots:
-                s.push(ctx, desc, layout, buf, i, grid, ncomp, like)
-        k = ks[-1] + 1
+        first = outs[0][0]
+        a0 = np.asarray(first.data, dtype=np.float64)
+        # two persistent pinned staging buffers per shape, alternating by
+        # batch: buffer b % 2 is rewritten only after batch b ran to the end
+        host = _pinned_stage((owner, parity, (len(ks),) + a0.shape))
+        hv = host.numpy()
+        for i, (f0, _) in enumerate(outs):
+            hv[i] = np.asarray(f0.data, dtype=np.float64)
+        return host, first
+
+    like = None
+    with cf.ThreadPoolExecutor(max_workers=1) as pool:
+        nxt = pool.submit(prepare, batches[0], 0) if batches else None
+        for b, ks in enumerate(batches):
+            host, first = nxt.result()
+            like = like or first
+            b0 = host.to("cuda", non_blocking=True)
+            nxt = pool.submit(prepare, batches[b + 1], (b + 1) % 2) if b + 1 < len(batches) else None
+            bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
+            run = DeviceRun(grid, cfg, bufs, len(ks), N.MODE_T_END, None, arith, log=False, ctx=ctx)
+            while True:
+                infos, done = run.poll()
+                if all(done):
+                    break
+                left = max(((cfg.t_end - i.t) / i.dt) if (i.dt > 0 and not d) else 1 for i, d in zip(infos, done))
+                run.steps(int(min(512, max(1, math.ceil(left) + 2))))
+            infos = run.end()
+            for j, info in zip(ks, infos):
+                if info.err:
+                    try:
+                        _raise_run_error(info, grid, ncomp)
+                    except E.ConslawError as exc:
+                        raise E.SimulationError(f"{where}sample {j} failed: {exc}") from exc
+            for i, j in enumerate(ks):
+                buf = bufs[int(infos[i].steps) % 2] if cfg.rk_order == 1 else bufs[0]
+                for s in slots:
+                    s.push(ctx, desc, layout, buf, i, grid, ncomp, like)
+    if evals:
+        evals.shutdown()
 
 
 @dataclass
@@ -523,7 +571,8 @@ def run_mlmc(plan, make_cfg, evaluate_init, workers: int = 1, *, batch: int | No
         grid_f = plan.grids[level]
         cfg_f = make_cfg(grid_f)
         slot = _Slot(FieldMoments(grid_f, cfg_f.model.ncomp), grid_f, cfg_f.model.ncomp)
-        _ensemble(plan, level, grid_f, cfg_f, evaluate_init, [slot], 0, plan.samples_per_level[level], batch, arith)
+        _ensemble(plan, level, grid_f, cfg_f, evaluate_init, [slot], 0, plan.samples_per_level[level], batch, arith,
+                  workers)
         acc_f = slot.gpu
         if level == 0:
             acc0 = acc_f
@@ -535,7 +584,7 @@ def run_mlmc(plan, make_cfg, evaluate_init, workers: int = 1, *, batch: int | No
             cfg_c = make_cfg(grid_c)
             slot_c = _Slot(FieldMoments(grid_c, cfg_c.model.ncomp), grid_c, cfg_c.model.ncomp)
             _ensemble(plan, level, grid_c, cfg_c, evaluate_init, [slot_c], 0, plan.samples_per_level[level], batch,
-                      arith)
+                      arith, workers)
             fc = slot_c.gpu
             factor_c = tuple(nf // nl for nf, nl in zip(finest.cells, grid_c.cells))
             mean_l = mean_l - prolong(fc._mean, factor_c)
