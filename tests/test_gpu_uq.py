@@ -123,3 +123,31 @@ def test_histogram_functional_matches_reference(P, golden):
     (res,) = uq.run_mc(uq.SamplePlan("mc", 8, 42, 4), grid, cfg, kelvin_helmholtz, [h], arith="exact")
     assert res.samples == case["samples"]
     assert res.counts.tolist() == case["counts"]
+
+
+@pytest.mark.parametrize("workers", [1, 3])
+def test_run_mc_workers_and_failing_sample(P, golden, workers):
+    """Concurrent initial-data evaluation (workers > 1, prefetched a batch
+    ahead) leaves the statistics bitwise unchanged, and a failing sample
+    raises the reference's message for the lowest failing index
+    (uq.py:281-288, pool.map order)."""
+    case = next(u for u in golden["uq"] if u["name"] == "kh2d128_mc8")
+    uq, grid, cfg, fn, plan, fm, sf = _setup(P, case)
+    m, s = uq.run_mc(plan, grid, cfg, fn, [fm, sf], workers=workers, batch=3, arith="exact")
+    assert O.sha16(m.acc.mean) == case["mean_sha"]
+    assert O.sha16(m.acc.variance(ddof=1)) == case["var_sha"]
+
+    seen = []
+
+    def bad(g, vec):
+        k = plan_vectors.index(tuple(vec))
+        seen.append(k)
+        if k in (5, 7):
+            raise ValueError(f"boom {k}")
+        return fn(g, vec)
+
+    plan_vectors = [tuple(uq.draw_sample(plan, k)) for k in range(plan.samples)]
+    with pytest.raises(P.SimulationError, match=r"^sample 5 failed: boom 5$"):
+        uq.run_mc(plan, grid, cfg, bad, [uq.FieldMoments(grid, cfg.model.ncomp)], workers=workers, batch=3,
+                  arith="exact")
+    assert 5 in seen
