@@ -200,6 +200,22 @@ int fvb_moments_merge(fvb_ctx* ctx, double* mean_a, double* m2_a, int64_t count_
 int fvb_structure_push(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay,
                        const double* u, int inst, int comp, double p, int H, double* d_sums);
 
+/* iodsl/expr.py:338-386 eval_init on the device: evaluate
+ * the per-component initial-data programs (stack bytecode compiled from the
+ * reference's expression AST by initdev.py; d_code / d_consts on the
+ * device, comp_off[ncomp+1] on the host) at every cell centre (origin[dim]
+ * + (i + 0.5) delta) of `ninst` samples (random vectors d_vecs, nrand per
+ * sample), convert primitive Euler data to conserved, and write the padded
+ * batch buffer `out` (ninst instances, ghosts zeroed).  d_bad[ninst *
+ * (ncomp + 2)] receives the lowest flat cell of: a non-finite component c,
+ * a non-positive primitive state (slot ncomp), an unphysical state (slot
+ * ncomp + 1); ~0 when none.  sin / cos / exp / pow are CUDA's: rounding-level
+ * parity with numpy, IEEE + - * / sqrt bitwise. */
+int fvb_init_eval(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, const double* origin,
+                  const int32_t* d_code, const int32_t* comp_off, const double* d_consts, int max_depth,
+                  int primitive, const double* d_vecs, int nrand, int ninst, double* out,
+                  unsigned long long* d_bad);
+
 /* parallel.py:185-254 halo slabs: pack the g-thick interior slab next to
  * face (axis, side) into a contiguous buffer / unpack a received slab into
  * the ghost region of that face.  Slabs span the full padded extent of the

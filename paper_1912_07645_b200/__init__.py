@@ -9,7 +9,7 @@ include/fvb200.h), driven from this Python layer with the reference's API.
 __version__ = "0.1.0"
 
 from .errors import (  # noqa: F401
-    ConfigError, ConslawError, ProtocolError, SimulationError, StaticFieldError, UnphysicalStateError,
+    ConfigError, ConslawError, ExprError, ProtocolError, SimulationError, StaticFieldError, UnphysicalStateError,
 )
 from .grid import BoundaryKind, Field, GridSpec, field_from_interior, fill_boundary, make_field, total_integral  # noqa: F401
 from .equations import EquationModel  # noqa: F401
@@ -18,3 +18,4 @@ from .solver import (  # noqa: F401
     DeviceField, SchemeConfig, TimeStepRecord, dt_from_maxima, run_simulation, spatial_residual,
     ssp_rk_advance, ssp_rk_step, stable_dt, wave_speed_maxima,
 )
+from .initdev import DeviceInit, parse_expr  # noqa: F401,E402

@@ -91,6 +91,9 @@ _SIGS = {
                            C.c_int64, C.c_int64], C.c_int),
     "fvb_structure_push": ([C.c_void_p, C.POINTER(Scheme), C.POINTER(Layout), C.c_void_p, C.c_int, C.c_int,
                             C.c_double, C.c_int, C.c_void_p], C.c_int),
+    "fvb_init_eval": ([C.c_void_p, C.POINTER(Scheme), C.POINTER(Layout), C.POINTER(C.c_double), C.c_void_p,
+                       C.POINTER(C.c_int32), C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
+                       C.c_void_p, C.c_void_p], C.c_int),
     "fvb_halo_pack": ([C.c_void_p, C.POINTER(Scheme), C.POINTER(Layout), C.c_void_p, C.c_int, C.c_int,
                        C.c_void_p], C.c_int),
     "fvb_halo_unpack": ([C.c_void_p, C.POINTER(Scheme), C.POINTER(Layout), C.c_void_p, C.c_int, C.c_int,
@@ -122,11 +125,18 @@ def load_library(path: Path | None = None) -> C.CDLL:
         return lib
 
 
+_CUDA_OK = False
+
+
 def _require_cuda():
+    global _CUDA_OK
+    if _CUDA_OK:  # a device stays visible once seen (is_available() queries the driver every call)
+        return
     import torch
 
     if not torch.cuda.is_available():
         raise NativeUnavailable("no CUDA device visible: the B200 hot path cannot run (no CPU fallback)")
+    _CUDA_OK = True
 
 
 class Context:

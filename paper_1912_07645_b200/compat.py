@@ -49,6 +49,6 @@ def install_into(pkg) -> dict:
     _sol.TYPES["Field"] = mods["grid"].Field
     _par.RankRecord = mods["parallel"].RankRecord
     for cls in ("ConfigError", "UnphysicalStateError", "SimulationError", "StaticFieldError", "ProtocolError",
-                "ConslawError"):
+                "ConslawError", "ExprError"):
         setattr(E, cls, getattr(mods["errors"], cls))
     return saved

@@ -299,6 +299,121 @@ __global__ void halo_instances_kernel(Pad p, fvb_layout L, double* u, int ncomp,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Device initial data: the reference's initial-data
+// expression language (iodsl/expr.py:338-386 eval_init) compiled on the host
+// into a stack bytecode (initdev.py) and evaluated per cell centre, for every
+// sample of a batch, straight into the padded batch buffer.  IEEE + - * / and
+// sqrt match numpy bitwise (this unit is built -fmad=false); sin / cos / exp
+// / pow are CUDA's (<= 2 ulp), so the result is rounding-level close to the
+// reference, not bitwise.
+// ---------------------------------------------------------------------------
+enum InitOp : int {
+  IO_CONST = 0, IO_X, IO_Y, IO_Z, IO_RAND, IO_NEG, IO_ADD, IO_SUB, IO_MUL, IO_DIV, IO_POW, IO_LT, IO_LE, IO_GT,
+  IO_GE, IO_EQ, IO_NE, IO_SEL, IO_SIN, IO_COS, IO_EXP, IO_ABS, IO_SQRT, IO_MIN, IO_MAX, IO_SQR, IO_RECIP
+};
+constexpr int kInitStack = 32;
+
+
+__device__ __forceinline__ double np_maximum(double a, double b) { return (a > b || a != a) ? a : b; }
+__device__ __forceinline__ double np_minimum(double a, double b) { return (a < b || a != a) ? a : b; }
+
+__device__ double init_run(const InitArgs& A, int c, const double* X, double cx, double cy, double cz) {
+  double st[kInitStack];
+  int sp = 0;
+  for (int i = A.off[c]; i < A.off[c + 1]; ++i) {
+    const int w = A.code[i];
+    const int op = w & 0xff, arg = w >> 8;
+    switch (op) {
+      case IO_CONST: st[sp++] = A.k[arg]; break;
+      case IO_X: st[sp++] = cx; break;
+      case IO_Y: st[sp++] = cy; break;
+      case IO_Z: st[sp++] = cz; break;
+      case IO_RAND: st[sp++] = X[arg]; break;
+      case IO_NEG: st[sp - 1] = -st[sp - 1]; break;
+      case IO_SIN: st[sp - 1] = sin(st[sp - 1]); break;
+      case IO_COS: st[sp - 1] = cos(st[sp - 1]); break;
+      case IO_EXP: st[sp - 1] = exp(st[sp - 1]); break;
+      case IO_ABS: st[sp - 1] = fabs(st[sp - 1]); break;
+      case IO_SQRT: st[sp - 1] = sqrt(st[sp - 1]); break;
+      case IO_SQR: st[sp - 1] = st[sp - 1] * st[sp - 1]; break;
+      case IO_RECIP: st[sp - 1] = 1.0 / st[sp - 1]; break;
+      case IO_SEL: {  // cond ? a : b  (np.where(cond != 0, a, b))
+        const double b = st[--sp], a = st[--sp], q = st[sp - 1];
+        st[sp - 1] = q != 0.0 ? a : b;
+        break;
+      }
+      default: {
+        const double b = st[--sp], a = st[sp - 1];
+        double r;
+        switch (op) {
+          case IO_ADD: r = a + b; break;
+          case IO_SUB: r = a - b; break;
+          case IO_MUL: r = a * b; break;
+          case IO_DIV: r = a / b; break;
+          case IO_POW: r = pow(a, b); break;
+          case IO_LT: r = a < b ? 1.0 : 0.0; break;
+          case IO_LE: r = a <= b ? 1.0 : 0.0; break;
+          case IO_GT: r = a > b ? 1.0 : 0.0; break;
+          case IO_GE: r = a >= b ? 1.0 : 0.0; break;
+          case IO_EQ: r = a == b ? 1.0 : 0.0; break;
+          case IO_NE: r = a != b ? 1.0 : 0.0; break;
+          case IO_MIN: r = np_minimum(a, b); break;
+          default: r = np_maximum(a, b); break;  // IO_MAX
+        }
+        st[sp - 1] = r;
+      }
+    }
+  }
+  return st[0];
+}
+
+// bad[inst * (ncomp + 2) + j]: lowest flat cell (numpy order) where
+// component j is non-finite (j < ncomp), the primitive state is
+// non-positive (j = ncomp), the conserved state is unphysical (ncomp + 1)
+__global__ void init_eval_kernel(InitArgs A, fvb_layout L, const double* vecs, int ninst, double* out,
+                                 unsigned long long* bad) {
+  const int64_t ncell = A.n[0] * A.n[1] * A.n[2];
+  const double floor_ = 1e-12;  // equations.py POSITIVITY_FLOOR
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncell * ninst;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int inst = (int)(i / ncell);
+    const int64_t cell = i - inst * ncell;
+    const int64_t x = cell % A.n[0], y = (cell / A.n[0]) % A.n[1], z = cell / (A.n[0] * A.n[1]);
+    // grid.py cell_centers: origin + (i + 0.5) * delta
+    const double cx = A.origin[0] + ((double)x + 0.5) * A.delta[0];
+    const double cy = A.dim >= 2 ? A.origin[1] + ((double)y + 0.5) * A.delta[1] : 0.0;
+    const double cz = A.dim >= 3 ? A.origin[2] + ((double)z + 0.5) * A.delta[2] : 0.0;
+    const double* X = vecs + (int64_t)inst * (A.nrand > 0 ? A.nrand : 1);
+    unsigned long long* b = bad + (int64_t)inst * (A.ncomp + 2);
+    double v[5];
+    for (int c = 0; c < A.ncomp; ++c) {
+      v[c] = init_run(A, c, X, cx, cy, cz);
+      if (!isfinite(v[c])) atomicMin(&b[c], (unsigned long long)cell);
+    }
+    if (A.euler) {
+      const int d = A.dim;
+      if (A.primitive) {  // equations.py:132-145 primitive_to_conserved
+        const double rho = v[0], p = v[1 + d];
+        if (rho <= floor_ || p <= floor_) atomicMin(&b[A.ncomp], (unsigned long long)cell);
+        double kin = 0.0;
+        for (int k = 0; k < d; ++k) {
+          kin = kin + v[1 + k] * v[1 + k];
+          v[1 + k] = rho * v[1 + k];
+        }
+        v[1 + d] = p / (A.gamma - 1.0) + 0.5 * rho * kin;
+      }
+      // equations.py:62-73 pressure / physical_mask
+      double msq = 0.0;
+      for (int k = 0; k < d; ++k) msq = msq + v[1 + k] * v[1 + k];
+      const double pr = (A.gamma - 1.0) * (v[1 + d] - msq / (2.0 * v[0]));
+      if (!(v[0] > floor_ && pr > floor_)) atomicMin(&b[A.ncomp + 1], (unsigned long long)cell);
+    }
+    double* o = out + inst * L.si + L.origin + x + y * L.sy + z * L.sz;
+    for (int c = 0; c < A.ncomp; ++c) o[c * L.sc] = v[c];
+  }
+}
+
 int grid_for(int64_t n) {
   int64_t b = (n + 255) / 256;
   if (b > 148 * 16) b = 148 * 16;
@@ -376,6 +491,13 @@ int launch_structure(const fvb_scheme& s, const fvb_layout& L, const double* u, 
   structure_pass1<<<nblocks, kSfThreads, 0, st>>>(p, L, u, inst, comp, pw, H, d_partials);
   structure_pass2<<<1, kSfThreads, 0, st>>>(d_partials, nblocks, H, s.dim, (double)(p.n[0] * p.n[1] * p.n[2]),
                                             d_sums);
+  return 0;
+}
+
+int launch_init_eval(const InitArgs& A, const fvb_layout& L, const double* vecs, int ninst, double* out,
+                     unsigned long long* bad, cudaStream_t st) {
+  const int64_t n = A.n[0] * A.n[1] * A.n[2] * ninst;
+  init_eval_kernel<<<grid_for(n), 256, 0, st>>>(A, L, vecs, ninst, out, bad);
   return 0;
 }
 

@@ -39,6 +39,8 @@ int launch_moments_merge(double* ma, double* m2a, int64_t ca, const double* mb, 
 int launch_structure(const fvb_scheme& s, const fvb_layout& L, const double* u, int inst, int comp, double p,
                      int H, double* d_sums, double* d_partials, int nblocks, cudaStream_t st);
 int structure_blocks(const fvb_scheme& s);
+int launch_init_eval(const InitArgs& A, const fvb_layout& L, const double* vecs, int ninst, double* out,
+                     unsigned long long* bad, cudaStream_t st);
 int launch_halo_instances(const fvb_scheme& s, const fvb_layout& L, double* u, int ninst, const int* ranks,
                           const int* periodic, cudaStream_t st);
 int launch_export(const FvbState* st, int dim, double* out, cudaStream_t s);
@@ -852,6 +854,39 @@ int fvb_structure_push(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay,
   fvb::launch_structure(*s, *lay, u, inst, comp, p, H, d_sums, ctx->d_partials, nb, ctx->stream);
   ctx->launches += 2;
   return check_launch(ctx, "structure_push");
+}
+
+int fvb_init_eval(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, const double* origin,
+                  const int32_t* d_code, const int32_t* comp_off, const double* d_consts, int max_depth,
+                  int primitive, const double* d_vecs, int nrand, int ninst, double* out,
+                  unsigned long long* d_bad) {
+  int r = validate(ctx, s);
+  if (r) return r;
+  if (max_depth < 1 || max_depth > 32)
+    return set_err(ctx, FVB_E_CONFIG, "initial-data expression needs a stack of %d (device limit 32)", max_depth);
+  if (ninst < 1) return set_err(ctx, FVB_E_CONFIG, "ninst must be >= 1");
+  fvb::InitArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.code = d_code;
+  A.k = d_consts;
+  for (int c = 0; c <= s->ncomp; ++c) A.off[c] = comp_off[c];
+  A.ncomp = s->ncomp;
+  A.dim = s->dim;
+  A.primitive = primitive;
+  A.euler = s->eq == FVB_EQ_EULER;
+  A.nrand = nrand;
+  A.gamma = s->gamma;
+  for (int k = 0; k < 3; ++k) {
+    A.origin[k] = k < s->dim ? origin[k] : 0.0;
+    A.delta[k] = k < s->dim ? s->deltas[k] : 1.0;
+    A.n[k] = k < s->dim ? s->cells[k] : 1;
+  }
+  // make_field(grid, ncomp, 0.0): ghosts are zero; error slots start at "none"
+  CUDA_TRY(ctx, cudaMemsetAsync(out, 0, sizeof(double) * lay->si * ninst, ctx->stream));
+  CUDA_TRY(ctx, cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long) * ninst * (s->ncomp + 2), ctx->stream));
+  fvb::launch_init_eval(A, *lay, d_vecs, ninst, out, d_bad, ctx->stream);
+  ctx->launches++;
+  return check_launch(ctx, "init_eval");
 }
 
 int fvb_halo_pack(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, const double* u, int axis, int side,

@@ -198,4 +198,14 @@ struct StageParams {
   LoopCtl ctl;
 };
 
+// Device initial-data program (fvb_aux.cu init_eval_kernel, initdev.py)
+struct InitArgs {
+  const int* code;     // all components' programs back to back; word = op | (arg << 8)
+  const double* k;     // constants
+  int off[9];          // program c = code[off[c] .. off[c+1])
+  int ncomp, dim, primitive, euler, nrand;
+  double origin[3], delta[3], gamma;
+  int64_t n[3];
+};
+
 }  // namespace fvb

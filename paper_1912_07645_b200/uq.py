@@ -497,14 +497,24 @@ def _ensemble(plan, level, grid, cfg, evaluate_init, slots, lo, hi, batch=None, 
             hv[i] = np.asarray(f0.data, dtype=np.float64)
         return host, first
 
+    from .initdev import DeviceInit
+
+    on_device = isinstance(evaluate_init, DeviceInit)  # initial data evaluated on the GPU: no host side at all
     like = None
     with cf.ThreadPoolExecutor(max_workers=1) as pool:
-        nxt = pool.submit(prepare, batches[0], 0) if batches else None
+        nxt = pool.submit(prepare, batches[0], 0) if batches and not on_device else None
         for b, ks in enumerate(batches):
-            host, first = nxt.result()
-            like = like or first
-            b0 = host.to("cuda", non_blocking=True)
-            nxt = pool.submit(prepare, batches[b + 1], (b + 1) % 2) if b + 1 < len(batches) else None
+            if on_device:
+                b0 = torch.empty((len(ks), ncomp) + tuple(grid.padded[::-1]), dtype=torch.float64, device="cuda")
+                errs = evaluate_init.evaluate_batch(grid, [draw_sample(plan, j, level) for j in ks], b0)
+                for j, exc in zip(ks, errs):
+                    if exc is not None:
+                        raise E.SimulationError(f"{where}sample {j} failed: {exc}") from exc
+            else:
+                host, first = nxt.result()
+                like = like or first
+                b0 = host.to("cuda", non_blocking=True)
+                nxt = pool.submit(prepare, batches[b + 1], (b + 1) % 2) if b + 1 < len(batches) else None
             bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
             run = DeviceRun(grid, cfg, bufs, len(ks), N.MODE_T_END, None, arith, log=False, ctx=ctx)
             while True:

@@ -31,7 +31,7 @@ from conslaw.equations import EquationModel  # noqa: E402
 from conslaw.errors import ConslawError  # noqa: E402
 from conslaw.grid import BoundaryKind, GridSpec, field_from_interior, fill_boundary  # noqa: E402
 from conslaw.iodsl.config import parse_config  # noqa: E402
-from conslaw.iodsl.expr import eval_init  # noqa: E402
+from conslaw.iodsl.expr import eval_expr, eval_init, parse_expr, print_expr  # noqa: E402
 from conslaw.numerics import FluxKind, Reconstruction, ReconstructionKind  # noqa: E402
 from conslaw.solver import SchemeConfig, run_simulation, spatial_residual, wave_speed_maxima  # noqa: E402
 from conslaw.uq import (FieldMoments, MlmcPlan, SamplePlan, StructureFunctionAccumulator, draw_sample,  # noqa: E402
@@ -279,6 +279,10 @@ def run_case(name, text, sample=0, max_steps=None, store=False, arrays=None, vec
         "dt_sha": sha(np.array([r.dt for r in recs])),
         "fallback_stages": fallbacks[0],
         "sum_final": [float(s) for s in final.interior.reshape(final.ncomp, -1).sum(axis=1)],
+        # the initial-data program, for the device evaluator (initdev.py)
+        "init_exprs": [print_expr(e) for e in rc.initial_exprs],
+        "primitive": bool(rc.initial_primitive),
+        "origin": [float(o) for o in rc.grid.origin],
     }
     if store and arrays is not None:
         arrays[f"{name}__init"] = np.asarray(init.data)
@@ -286,6 +290,28 @@ def run_case(name, text, sample=0, max_steps=None, store=False, arrays=None, vec
         arrays[f"{name}__dt"] = np.array([r.dt for r in recs])
     print(f"{name}: steps={case['steps']} final={case['final_sha']} fallbacks={fallbacks[0]}")
     return case
+
+
+EXPR_TEXTS = [
+    "1 + 2*x", "-x^2", "(y < 0.25 + 0.01*sin(2*pi*x)) ? 2 : 1", "max(x, -y) ^ 0.5 / exp(-X0)",
+    "1 < 2 == 3 >= 4", "2^3^2", "-(-x)", "x ? y ? 1 : 2 : z", ".5e-3*x - 3e2", "abs(min(1,2))",
+    "x^-1 + (x - 0.5)^2 * y^0.5", "cos(x) != sin(y) ? sqrt(abs(x - y)) : -1.5e+1", "X3 * (X1 - 0.5) <= x",
+    "((x))", "1 - 2 - 3 / 4 / 5 * 6",
+]
+
+
+def expr_cases():
+    """Parser / printer fingerprints and pointwise values of the reference's
+    expression language (iodsl/expr.py) on a few points."""
+    xs = np.array([0.1, 0.37, 0.5, 0.81])
+    env = {"x": xs, "y": xs[::-1].copy(), "z": xs * 0.5, "X0": 0.3, "X1": 0.7, "X2": 0.1, "X3": 0.9}
+    out = []
+    for t in EXPR_TEXTS:
+        node = parse_expr(t)
+        val = np.broadcast_to(np.asarray(eval_expr(node, env), dtype=float), xs.shape)
+        out.append({"text": t, "print": print_expr(node), "repr": repr(node).replace("conslaw.iodsl.expr.", ""),
+                    "values": [float(v) for v in val]})
+    return out
 
 
 def residual_cases(arrays):
@@ -540,6 +566,7 @@ def main():
             eq=eq, recon=recon, rk=rk, bc=bc, speed="advection_speed = 0.7 -0.4 0.5\n" if eq == "advection" else ""), store=True, arrays=arrays))
     runs.append(run_case("euler3d_tiles_hllc_weno2", EULER_3D_TILES, store=True, arrays=arrays))
 
+    gold["exprs"] = expr_cases()
     gold["residuals"] = residual_cases(arrays)
     gold["errors"] = error_cases()
 

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--workers", type=int, default=1)
     ap.add_argument("--cached-init", action="store_true", help="evaluate_init returns one precomputed field")
+    ap.add_argument("--device-init", action="store_true", help="initial data evaluated on the GPU (DeviceInit)")
     a = ap.parse_args()
     n = a.cells
     grid = P.GridSpec(2, (n, n), (0.0, 0.0), (1.0, 1.0), ghost_width=2)
@@ -42,6 +43,11 @@ def main():
         t_init[0] += time.perf_counter() - t0
         return f
 
+    if a.device_init:  # the KH2D preset program, evaluated by fvb_init_eval
+        kh = ["y < 0.25 + 0.01 * sin(2.0 * pi * (x + X0)) ? 1.0 : y < 0.75 + 0.01 * sin(2.0 * pi * (x + X1)) ? 2.0 : 1.0",
+              "y < 0.25 + 0.01 * sin(2.0 * pi * (x + X2)) ? -0.5 : y < 0.75 + 0.01 * sin(2.0 * pi * (x + X3)) ? 0.5 : -0.5",
+              "0.0", "2.5"]
+        init = P.DeviceInit(kh, cfg.model, primitive=True)
     # warm (kernels, allocator)
     uq.run_mc(uq.SamplePlan("mc", 2, 42, 4), grid, cfg, init, [uq.FieldMoments(grid, 4)], arith="fast")
     t_init[0] = 0.0
