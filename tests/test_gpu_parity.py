@@ -151,6 +151,24 @@ def test_observers_sequence(P, golden, golden_arrays):
     assert seen[-1][2] == O.sha16(final.interior)
 
 
+def test_observer_fields_kept_past_the_call(P, golden, golden_arrays):
+    """Observer fields are lazily copied to the host: one kept and read after
+    later steps still holds its own step's state (zero ghosts, caller's type)."""
+    case = next(r for r in golden["runs"] if r["name"] == "kh2d64_weno2_50")
+    grid, cfg = product_objects(case["scheme"])
+    init = _init_field(P, case, golden_arrays, grid)
+    kept = []
+    P.run_simulation(init, cfg, observers=[lambda s, t, f: kept.append((s, f))], max_steps=6, arith="exact")
+    sc = oracle_scheme(case["scheme"])
+    for step in (0, 1, 3, 6):
+        s, f = kept[step]
+        assert s == step and isinstance(f, type(init))
+        ref, _ = O.simulate(init.data, sc, step) if step else (init.data, None)
+        assert O.sha16(f.interior) == O.sha16(O.interior(ref, sc)), step
+        g = grid.ghost_width
+        assert not f.data[:, :g].any() and not f.data[:, :, -g:].any()
+
+
 def test_device_field_roundtrip(P, golden, golden_arrays):
     case = next(r for r in golden["runs"] if r["name"] == "kh2d64_weno2_50")
     grid, cfg = product_objects(case["scheme"])
