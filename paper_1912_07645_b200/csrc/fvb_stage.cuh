@@ -1000,7 +1000,10 @@ constexpr int ring_smem_bytes() {
 #ifndef FVB_RING3_MINB
 #define FVB_RING3_MINB 2
 #endif
-constexpr int kRing3NT = 32, kRing3NTY = 8, kRing3Slots = 4;
+#ifndef FVB_RING3_NTY
+#define FVB_RING3_NTY 8
+#endif
+constexpr int kRing3NT = 32, kRing3NTY = FVB_RING3_NTY, kRing3Slots = 4;
 
 template <int EQ, int FLUX, int RECON, bool FIN>
 __global__ void __launch_bounds__(kRing3NT * kRing3NTY, FVB_RING3_MINB)
