@@ -371,10 +371,13 @@ __device__ __forceinline__ void hllc(const double* uL, const double* uR, const E
     euler_flux<DIM>(uL, L.p, L.v, axis, F);
     return;
   }
-  const double den = L.rho * (sL - L.v) - R.rho * (sR - R.v);
 #if FVB_FAST
-  const double sM = fdiv(fma(L.rho * L.v, sL - L.v, R.p - L.p) - R.rho * R.v * (sR - R.v), den);
+  // rho v is the momentum itself: sM = (pR - pL + mL (sL - vL) - mR (sR - vR)) / den
+  const double aL = sL - L.v, aR = sR - R.v;
+  const double den = fma(L.rho, aL, -R.rho * aR);
+  const double sM = fdiv(fma(-uR[1 + axis], aR, fma(uL[1 + axis], aL, R.p - L.p)), den);
 #else
+  const double den = L.rho * (sL - L.v) - R.rho * (sR - R.v);
   const double sM = (R.p - L.p + L.rho * L.v * (sL - L.v) - R.rho * R.v * (sR - R.v)) / den;
 #endif
   const bool left = equal || (sL >= 0.0) || (sM >= 0.0);
