@@ -187,6 +187,14 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
   if (s.arith == FVB_ARITH_FAST) fvb::fast::stage_block(s.dim, p.variant, nt, nty);
   else fvb::exact::stage_block(s.dim, p.variant, nt, nty);
   const int64_t strips = (p.n[0] + (nt - 2) - 1) / (nt - 2);
+  // batched scalar ensembles on the 2D ring kernel: two instances per block
+  p.ni = 1;
+  if (s.dim == 2 && p.variant == 2 && s.ncomp == 1 && ninst % 2 == 0 && !p.shared_state) {
+    const char* e = getenv("FVB_RING_NI");
+    const int want = e ? atoi(e) : 2;
+    p.ni = (want == 4 && ninst % 4 == 0) ? 4 : (want == 1 ? 1 : 2);
+  }
+  const int nig = ninst / p.ni;  // instance groups along grid z
   dim3 g(1, 1, 1);
   g.x = (unsigned)strips;
   int64_t H = 1, chunks = 1;
@@ -206,7 +214,7 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
     if (const char* e = getenv("FVB_BLOCKS_PER_SM")) per_sm = std::max(1, atoi(e));
     if (const char* e = getenv("FVB_WAVES")) waves = std::max(1, atoi(e));
     const int64_t slots = 148 * per_sm;
-    const int64_t base = strips * ytiles * ninst;
+    const int64_t base = strips * ytiles * nig;
     int64_t want_chunks = 1;
     if (getenv("FVB_WAVES")) {
       want_chunks = (slots * waves + base - 1) / base;
@@ -230,7 +238,7 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
     chunks = (nm + H - 1) / H;
     if (s.dim == 2) {
       g.y = (unsigned)chunks;
-      g.z = ninst;
+      g.z = nig;
     } else {
       g.y = (unsigned)ytiles;
       g.z = (unsigned)(chunks * ninst);

@@ -59,6 +59,18 @@ static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
   if constexpr (DIM == 2) {
     if (p.variant == 2) {
       constexpr int NT = kRingNT;
+      if constexpr (NComp<EQ, 2>::value == 1) {
+        if (p.ni == 2) {  // two instances per block (batched scalar ensembles)
+          const int smem = ring_smem_bytes<EQ, RECON, NT, 2>() + 8 * (p.H + kRingPD + 4);
+          ring_kernel<EQ, FLUX, RECON, NT, FIN, 2><<<grid, NT, smem, s>>>(p);
+          return 0;
+        }
+        if (p.ni == 4) {
+          const int smem = ring_smem_bytes<EQ, RECON, NT, 4>() + 8 * (p.H + kRingPD + 4);
+          ring_kernel<EQ, FLUX, RECON, NT, FIN, 4><<<grid, NT, smem, s>>>(p);
+          return 0;
+        }
+      }
       const int smem = ring_smem_bytes<EQ, RECON, NT>() + 8 * (p.H + kRingPD + 4);  // + row-offset table
       ring_kernel<EQ, FLUX, RECON, NT, FIN><<<grid, NT, smem, s>>>(p);
       return 0;

@@ -768,11 +768,17 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 constexpr int kRingPD = 2;               // rows in flight ahead of the consumer
 constexpr int kRingRows = kRingPD + 3;   // ring slots
 
-template <int EQ, int FLUX, int RECON, int NT, bool FIN>
+// NI > 1 (scalar laws, batched ensembles): one block marches the same
+// strip of NI instances at once -- the instances are "virtual components"
+// (component stride = instance stride), so the row bookkeeping, barriers
+// and copies are shared and the per-instance math interleaves.
+template <int EQ, int FLUX, int RECON, int NT, bool FIN, int NI = 1>
 __global__ void __launch_bounds__(NT, FVB_RING_MINB)
 ring_kernel(const StageParams p) {
   constexpr int DIM = 2;
-  constexpr int NC = NComp<EQ, DIM>::value;
+  constexpr int NCP = NComp<EQ, DIM>::value;  // physical components
+  static_assert(NI == 1 || NCP == 1, "instance batching is for scalar laws");
+  constexpr int NC = NCP * NI;                // components held per cell here
   constexpr bool WENO = RECON != RECON_NONE;
   constexpr int W = NT + 2;
   extern __shared__ double smem[];
@@ -788,10 +794,22 @@ ring_kernel(const StageParams p) {
   auto RG = [&](int slot, int c, int x) -> double& { return ring[(slot * NC + c) * W + x]; };
   auto NR = [&](int slot, int c) -> double& { return nring[(slot * NC + c) * NT + threadIdx.x]; };
 
-  const int inst = blockIdx.z;
+  const int inst = blockIdx.z * NI;
   FvbState* st = p.st + (p.shared_state ? 0 : inst);
-  if (*(volatile int*)&st->done) return;
-  const double dt = p.kind == 0 ? 0.0 : *(volatile double*)&st->dt;
+  FvbState* sts[NI];
+  double dts[NI];
+  bool act[NI];
+  bool any = false;
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    sts[i] = p.st + (p.shared_state ? 0 : inst + i);
+    act[i] = !*(volatile int*)&sts[i]->done;
+    any = any || act[i];
+    dts[i] = p.kind == 0 ? 0.0 : *(volatile double*)&sts[i]->dt;
+  }
+  if (!any) return;
+  const double dt = dts[0];
+  const int64_t cs = NI > 1 ? p.si : p.sc;  // stride between the components held here
   const double* __restrict__ us = p.us + p.origin + inst * p.si;
   const double* un = p.un + p.origin + inst * p.si;
   double* out = p.out + p.origin + inst * p.si;
@@ -814,15 +832,20 @@ ring_kernel(const StageParams p) {
   auto fetch = [&](int64_t r, int slot) {  // async copy of row r into a ring slot
     const int64_t ro = roff(r);
 #pragma unroll
-    for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, tx + 1), us + co + ro + c * p.sc);
+    for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, tx + 1), us + co + ro + c * cs);
     if (halo_t) {
 #pragma unroll
-      for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, hcol), us + hco + ro + c * p.sc);
+      for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, hcol), us + hco + ro + c * cs);
     }
   };
 
-  unsigned errb = 0;
-  double smax[DIM] = {0.0, 0.0};
+  unsigned errb = 0, errbs[NI];
+  double smax[DIM] = {0.0, 0.0}, smaxs[NI][DIM];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    errbs[i] = 0;
+    smaxs[i][0] = smaxs[i][1] = 0.0;
+  }
   // RK stage as a*u^n + b*(u^s + dt L) (solver.py:166-173); fast mode only
   const double rk_a = p.kind == 2 ? 0.5 : (p.kind == 3 ? 0.75 : (p.kind == 4 ? 1.0 / 3.0 : 0.0));
   const double rk_b = p.kind == 2 ? 0.5 : (p.kind == 3 ? 0.25 : (p.kind == 4 ? 2.0 / 3.0 : 1.0));
@@ -849,7 +872,7 @@ ring_kernel(const StageParams p) {
         const int64_t o = co + roff(r + 1);
         const int ns = (int)((r + 1 - ra) % 3);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) cp_async8(&NR(ns, c), un + o + c * p.sc);
+        for (int c = 0; c < NC; ++c) cp_async8(&NR(ns, c), un + o + c * cs);
       }
       cp_async_commit();
     }
@@ -880,9 +903,18 @@ ring_kernel(const StageParams p) {
         double GC[NC], H[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) H[c] = hs[c * NT + tx];
-        unsigned eb = 0;
-        interface_flux<EQ, FLUX, DIM, RECON>(H, lo, A, B, 1, p.P, GC, eb);
-        if (eb && cell) errb |= 2u;
+        if constexpr (NI == 1) {
+          unsigned eb = 0;
+          interface_flux<EQ, FLUX, DIM, RECON>(H, lo, A, B, 1, p.P, GC, eb);
+          if (eb && cell) errb |= 2u;
+        } else {
+#pragma unroll
+          for (int i = 0; i < NI; ++i) {
+            unsigned eb = 0;
+            interface_flux<EQ, FLUX, DIM, RECON>(H + i, lo + i, A + i, B + i, 1, p.P, GC + i, eb);
+            if (eb && cell) errbs[i] |= 2u;
+          }
+        }
         double v[NC];
         const int tr = tx + 1 < NT ? tx + 1 : NT - 1;
 #pragma unroll
@@ -895,16 +927,26 @@ ring_kernel(const StageParams p) {
           const double Lc = (0.0 - ddiv(g1 - g0, p, 0)) - ddiv(GC[c] - Gp, p, 1);
 #endif
 #if FVB_FAST
-          v[c] = p.kind == 0 ? Lc : fma(rk_a, unc[c], rk_b * fma(dt, Lc, A[c]));
+          v[c] = p.kind == 0 ? Lc : fma(rk_a, unc[c], rk_b * fma(NI > 1 ? dts[c] : dt, Lc, A[c]));
 #else
-          v[c] = rk_combine(p.kind, unc[c], A[c], dt, Lc);
+          v[c] = rk_combine(p.kind, unc[c], A[c], NI > 1 ? dts[c] : dt, Lc);
 #endif
         }
         if (fin) {
           const int64_t o = co + roff(r - 1);
+          if constexpr (NI == 1) {
 #pragma unroll
-          for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
-          if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v, xf, r - 1, 0, smax);
+            for (int c = 0; c < NC; ++c) out[o + c * cs] = v[c];
+            if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v, xf, r - 1, 0, smax);
+          } else {
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+              if (act[i]) {
+                out[o + i * cs] = v[i];
+                if constexpr (FIN) post_cell<EQ, DIM, NCP>(p, sts[i], v + i, xf, r - 1, 0, smaxs[i]);
+              }
+            }
+          }
         }
 #pragma unroll
         for (int c = 0; c < NC; ++c) gs[c * NT + tx] = GC[c];
@@ -947,16 +989,25 @@ ring_kernel(const StageParams p) {
           uL[c] = WENO ? hx[c * NT + tl] : RG(sB, c, tx);
           uR[c] = WENO ? lx[c * NT + tx] : RG(sB, c, tx + 1);
         }
-        auto cells = [&](double* a, double* b) {  // fallback only: loaded on demand
+        if constexpr (NI == 1) {
+          auto cells = [&](double* a, double* b) {  // fallback only: loaded on demand
 #pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            a[c] = RG(sB, c, tx);
-            b[c] = RG(sB, c, tx + 1);
+            for (int c = 0; c < NC; ++c) {
+              a[c] = RG(sB, c, tx);
+              b[c] = RG(sB, c, tx + 1);
+            }
+          };
+          unsigned eb = 0;
+          interface_flux_lazy<EQ, FLUX, DIM, RECON>(uL, uR, cells, 0, p.P, Gx, eb);
+          if (eb && tx >= 1 && xf <= p.n[0]) errb |= 1u;
+        } else {  // scalar laws: no positivity fallback, the cells are never read
+#pragma unroll
+          for (int i = 0; i < NI; ++i) {
+            unsigned eb = 0;
+            interface_flux<EQ, FLUX, DIM, RECON>(uL + i, uR + i, uL + i, uR + i, 0, p.P, Gx + i, eb);
+            if (eb && tx >= 1 && xf <= p.n[0]) errbs[i] |= 1u;
           }
-        };
-        unsigned eb = 0;
-        interface_flux_lazy<EQ, FLUX, DIM, RECON>(uL, uR, cells, 0, p.P, Gx, eb);
-        if (eb && tx >= 1 && xf <= p.n[0]) errb |= 1u;
+        }
 #pragma unroll
         for (int c = 0; c < NC; ++c) gx[c * NT + tx] = Gx[c];
       }
@@ -966,18 +1017,32 @@ ring_kernel(const StageParams p) {
     sA = sB;
   }
   cp_async_wait<0>();
-  if (errb) {
+  if constexpr (NI == 1) {
+    if (errb) {
 #pragma unroll
-    for (int a = 0; a < DIM; ++a)
-      if (errb & (1u << a))
-        atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | ((long long)(1 + a) << 40));
+      for (int a = 0; a < DIM; ++a)
+        if (errb & (1u << a))
+          atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | ((long long)(1 + a) << 40));
+    }
+    if constexpr (FIN) block_epilogue<DIM>(p, st, inst, smax, true);
+  } else {
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      if (!act[i]) continue;  // block-uniform
+      if (errbs[i]) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a)
+          if (errbs[i] & (1u << a))
+            atomicMin(&sts[i]->stage_err, ((long long)p.stage_idx << 42) | ((long long)(1 + a) << 40));
+      }
+      if constexpr (FIN) block_epilogue<DIM>(p, sts[i], inst + i, smaxs[i], true);
+    }
   }
-  if constexpr (FIN) block_epilogue<DIM>(p, st, inst, smax, true);
 }
 
-template <int EQ, int RECON, int NT>
+template <int EQ, int RECON, int NT, int NI = 1>
 constexpr int ring_smem_bytes() {
-  constexpr int NC = NComp<EQ, 2>::value;
+  constexpr int NC = NComp<EQ, 2>::value * NI;
   return 8 * (kRingRows * NC * (NT + 2) + (RECON != RECON_NONE ? 2 : 0) * NC * NT + NC * NT + 3 * NC * NT +
               2 * NC * NT);
 }

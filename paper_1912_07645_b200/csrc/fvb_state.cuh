@@ -194,6 +194,7 @@ struct StageParams {
   int shared_state;   // 1: all instances are subdomains of one run (one FvbState)
   int defer_finalize; // 1: leave maxima/flags in the state; the caller reduces them
                       //    across ranks and calls fvb_run_finalize
+  int ni;             // instances per block (2D ring kernel, scalar laws); 0/1 = one
   int variant;        // 1D/2D kernel: 0 = warp strip, 1 = shared-memory tile
   LoopCtl ctl;
 };

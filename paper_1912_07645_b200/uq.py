@@ -383,8 +383,12 @@ def shard_range(n: int, world: int, rank: int):
 
 
 def default_batch(grid, ncomp: int) -> int:
+    """Samples per device batch: ~16M cell-components (KH2D 512^2: 16,
+    Burgers 2048^2: 4), at most 64; even when possible (the scalar ring
+    kernel marches two instances per block)."""
     cells = math.prod(grid.cells)
-    return int(max(1, min(64, (4 << 20) // max(1, cells))))
+    b = int(max(1, min(64, (16 << 20) // max(1, cells * ncomp))))
+    return b - (b % 2) if b > 1 else b
 
 
 def run_mc(plan, grid, cfg, evaluate_init, functionals, workers: int = 1, *, batch: int | None = None,
