@@ -151,3 +151,15 @@ def test_run_mc_workers_and_failing_sample(P, golden, workers):
         uq.run_mc(plan, grid, cfg, bad, [uq.FieldMoments(grid, cfg.model.ncomp)], workers=workers, batch=3,
                   arith="exact")
     assert 5 in seen
+
+
+@pytest.mark.parametrize("ni", ["1", "2", "4"])
+def test_scalar_instances_per_block_bitwise(P, golden, monkeypatch, ni):
+    """The scalar ring kernel marching 1, 2 or 4 ensemble instances per block
+    (FVB_RING_NI) gives the reference's statistics bitwise."""
+    monkeypatch.setenv("FVB_RING_NI", ni)
+    case = next(u for u in golden["uq"] if u["name"] == "burgers128_qmc8")
+    uq, grid, cfg, fn, plan, fm, sf = _setup(P, case)
+    m, s = uq.run_mc(plan, grid, cfg, fn, [fm, sf], batch=4, arith="exact")
+    assert O.sha16(m.acc.mean) == case["mean_sha"]
+    assert O.sha16(m.acc.variance(ddof=1)) == case["var_sha"]
