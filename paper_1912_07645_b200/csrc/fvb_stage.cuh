@@ -1210,31 +1210,28 @@ ring3_kernel(const StageParams p) {
         }
       }
       // ---- x sweep (interior face rows) ----
-      if constexpr (WENO) {
-        if (inrow) {
-          double um[NC], uc[NC], up[NC], hi[NC], lo[NC];
+      // A warp is one face row of the tile (32 consecutive x cells), so the
+      // x neighbours are lanes of the same warp: faces and fluxes move by
+      // shuffle, with no shared-memory round trip and no barrier.
+      if (inrow) {  // warp-uniform; x interface tx sits between face cells tx-1 and tx (lane 0's is unused)
+        double uL[NC], uR[NC], G[NC];
+        if constexpr (WENO) {
+          double um[NC], uc[NC], up[NC], hi[NC];
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
             um[c] = RG(sB, c, ty + 1, tx);
             uc[c] = RG(sB, c, ty + 1, tx + 1);
             up[c] = RG(sB, c, ty + 1, tx + 2);
           }
-          weno_faces_nc<NC, RECON>(um, uc, up, p.P.eps, hi, lo);
+          weno_faces_nc<NC, RECON>(um, uc, up, p.P.eps, hi, uR);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) uL[c] = __shfl_up_sync(0xffffffffu, hi[c], 1);
+        } else {
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
-            hf[FI(c, ty, tx)] = hi[c];
-            lf[FI(c, ty, tx)] = lo[c];
+            uL[c] = RG(sB, c, ty + 1, tx);
+            uR[c] = RG(sB, c, ty + 1, tx + 1);
           }
-        }
-        __syncthreads();
-      }
-      if (inrow) {  // x interface tx sits between face cells tx-1 and tx (lane 0's is unused)
-        const int tl = tx >= 1 ? tx - 1 : 0;
-        double uL[NC], uR[NC], G[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          uL[c] = WENO ? hf[FI(c, ty, tl)] : RG(sB, c, ty + 1, tx);
-          uR[c] = WENO ? lf[FI(c, ty, tx)] : RG(sB, c, ty + 1, tx + 1);
         }
         auto cells = [&](double* a, double* b) {  // fallback only: loaded on demand
 #pragma unroll
@@ -1247,17 +1244,12 @@ ring3_kernel(const StageParams p) {
         interface_flux_lazy<EQ, FLUX, DIM, RECON>(uL, uR, cells, 0, p.P, G, eb);
         if (eb && tx >= 1 && xf <= p.n[0] && yf < p.n[1]) errb |= 1u;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) gf[FI(c, ty, tx)] = G[c];
-      }
-      __syncthreads();
-      if (inrow) {
-        const int tr = tx + 1 < NT ? tx + 1 : NT - 1;
-#pragma unroll
         for (int c = 0; c < NC; ++c) {
+          const double Gr = __shfl_down_sync(0xffffffffu, G[c], 1);  // lane 31's is unused
 #if FVB_FAST
-          R[c] = (gf[FI(c, ty, tx)] - gf[FI(c, ty, tr)]) * p.id[0];
+          R[c] = (G[c] - Gr) * p.id[0];
 #else
-          R[c] = 0.0 - ddiv(gf[FI(c, ty, tr)] - gf[FI(c, ty, tx)], p, 0);
+          R[c] = 0.0 - ddiv(Gr - G[c], p, 0);
 #endif
         }
       }
@@ -1277,7 +1269,7 @@ ring3_kernel(const StageParams p) {
           lf[FI(c, ty, tx)] = lo[c];
         }
       }
-      __syncthreads();  // y faces visible; every x residual read of gf done
+      __syncthreads();  // y faces visible
       if (ty >= 1) {  // y interface ty sits between face rows ty-1 and ty
         double uL[NC], uR[NC], G[NC];
 #pragma unroll
