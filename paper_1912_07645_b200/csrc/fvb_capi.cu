@@ -20,12 +20,12 @@ namespace fvb {
 namespace exact {
 int launch_stage(int dim, int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s);
 int launch_speed(int dim, int eq, const StageParams& p, int finalize, dim3 grid, cudaStream_t s);
-void stage_block(int dim, int variant, int& nt, int& nty);
+void stage_block(int dim, int eq, int variant, int& nt, int& nty);
 }  // namespace exact
 namespace fast {
 int launch_stage(int dim, int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s);
 int launch_speed(int dim, int eq, const StageParams& p, int finalize, dim3 grid, cudaStream_t s);
-void stage_block(int dim, int variant, int& nt, int& nty);
+void stage_block(int dim, int eq, int variant, int& nt, int& nty);
 }  // namespace fast
 // fvb_aux.cu
 int launch_fill_axis(const fvb_scheme& s, const fvb_layout& L, double* u, int ninst, int axis, cudaStream_t st);
@@ -184,8 +184,8 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
   if (kv && std::strcmp(kv, "strip") == 0) p.variant = 0;
   if (kv && std::strcmp(kv, "tile") == 0) p.variant = 1;
   if (s.dim == 1 && p.variant == 2) p.variant = 1;
-  if (s.arith == FVB_ARITH_FAST) fvb::fast::stage_block(s.dim, p.variant, nt, nty);
-  else fvb::exact::stage_block(s.dim, p.variant, nt, nty);
+  if (s.arith == FVB_ARITH_FAST) fvb::fast::stage_block(s.dim, s.eq, p.variant, nt, nty);
+  else fvb::exact::stage_block(s.dim, s.eq, p.variant, nt, nty);
   const int64_t strips = (p.n[0] + (nt - 2) - 1) / (nt - 2);
   // batched scalar ensembles on the 2D ring kernel: two instances per block
   p.ni = 1;

@@ -19,12 +19,17 @@ constexpr int kStripWarps = 4;
 #ifndef FVB_RING_NT
 #define FVB_RING_NT 64
 #endif
-constexpr int kRingNT = FVB_RING_NT;
+#ifndef FVB_RING_NT_SCALAR
+#define FVB_RING_NT_SCALAR 32
+#endif
+// Euler: two-warp blocks; scalar laws: one-warp blocks whose x sweep runs on
+// shuffles (measured: Euler 19.2 vs 15.5 at 32, Burgers 107.5 vs 114 at 32)
+constexpr int kRingNT = FVB_RING_NT, kRingNTScalar = FVB_RING_NT_SCALAR;
 
 // cells per block along x (reported as nt-2) and the y tile (nty-2, 3D only)
-void stage_block(int dim, int variant, int& nt, int& nty) {
+void stage_block(int dim, int eq, int variant, int& nt, int& nty) {
   if (dim == 1 && variant == 2) variant = 1;
-  if (dim == 2 && variant == 2) { nt = kRingNT; nty = 1; return; }
+  if (dim == 2 && variant == 2) { nt = eq == EQ_EULER ? kRingNT : kRingNTScalar; nty = 1; return; }
   if (dim == 3 && variant == 2) { nt = kRing3NT; nty = kRing3NTY; return; }
   if (dim <= 2 && variant == 0) { nt = kStripCells * kStripWarps + 2; nty = 1; }
   else if (dim == 1) { nt = Blk<1>::NT; nty = 1; }
@@ -58,7 +63,7 @@ static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
   }
   if constexpr (DIM == 2) {
     if (p.variant == 2) {
-      constexpr int NT = kRingNT;
+      constexpr int NT = NComp<EQ, 2>::value == 1 ? kRingNTScalar : kRingNT;
       if constexpr (NComp<EQ, 2>::value == 1) {
         if (p.ni == 2) {  // two instances per block (batched scalar ensembles)
           const int smem = ring_smem_bytes<EQ, RECON, NT, 2>() + 8 * (p.H + kRingPD + 4);

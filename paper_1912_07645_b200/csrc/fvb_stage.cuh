@@ -747,13 +747,6 @@ strip_kernel(const StageParams p) {
 // row straight from the ring (no staging store), and the 24 window
 // registers are freed for occupancy.
 // ---------------------------------------------------------------------------
-#ifndef FVB_RING_NT_FOR_MINB
-#ifdef FVB_RING_NT
-#define FVB_RING_NT_FOR_MINB FVB_RING_NT
-#else
-#define FVB_RING_NT_FOR_MINB 64
-#endif
-#endif
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
@@ -763,7 +756,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 #ifndef FVB_RING_MINB
-#define FVB_RING_MINB (512 / FVB_RING_NT_FOR_MINB)
+#define FVB_RING_MINB (512 / NT)  // 16 warps/SM at 128 registers
 #endif
 constexpr int kRingPD = 2;               // rows in flight ahead of the consumer
 constexpr int kRingRows = kRingPD + 3;   // ring slots
@@ -779,6 +772,9 @@ ring_kernel(const StageParams p) {
   constexpr int NCP = NComp<EQ, DIM>::value;  // physical components
   static_assert(NI == 1 || NCP == 1, "instance batching is for scalar laws");
   constexpr int NC = NCP * NI;                // components held per cell here
+  // one-warp blocks: the x neighbours are lanes of the warp -> the x sweep
+  // runs on shuffles, and gx holds each column's own x residual
+  constexpr bool kShflX = NT == 32;
   constexpr bool WENO = RECON != RECON_NONE;
   constexpr int W = NT + 2;
   extern __shared__ double smem[];
@@ -920,11 +916,22 @@ ring_kernel(const StageParams p) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           // x residual of row r-1 straight from its fluxes (still in gx)
-          const double g0 = gx[c * NT + tx], g1 = gx[c * NT + tr], Gp = gs[c * NT + tx];
+          const double Gp = gs[c * NT + tx];
+          double xres;
+          if constexpr (kShflX) {
+            xres = gx[c * NT + tx];  // this column's own, computed by the x sweep
+          } else {
+            const double g0 = gx[c * NT + tx], g1 = gx[c * NT + tr];
 #if FVB_FAST
-          const double Lc = fma(Gp - GC[c], p.id[1], (g0 - g1) * p.id[0]);
+            xres = (g0 - g1) * p.id[0];
 #else
-          const double Lc = (0.0 - ddiv(g1 - g0, p, 0)) - ddiv(GC[c] - Gp, p, 1);
+            xres = 0.0 - ddiv(g1 - g0, p, 0);
+#endif
+          }
+#if FVB_FAST
+          const double Lc = fma(Gp - GC[c], p.id[1], xres);
+#else
+          const double Lc = xres - ddiv(GC[c] - Gp, p, 1);
 #endif
 #if FVB_FAST
           v[c] = p.kind == 0 ? Lc : fma(rk_a, unc[c], rk_b * fma(NI > 1 ? dts[c] : dt, Lc, A[c]));
@@ -964,6 +971,55 @@ ring_kernel(const StageParams p) {
             atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | flat_cell<DIM>(p, xf, r, 0));
         }
       }
+      if constexpr (kShflX) {  // x sweep on shuffles: no shared-memory faces, no barrier
+        double uL[NC], uR[NC], Gx[NC];
+        if constexpr (WENO) {
+          double um[NC], uc[NC], up[NC], hi[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            um[c] = RG(sB, c, tx);
+            uc[c] = RG(sB, c, tx + 1);
+            up[c] = RG(sB, c, tx + 2);
+          }
+          weno_faces_nc<NC, RECON>(um, uc, up, p.P.eps, hi, uR);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) uL[c] = __shfl_up_sync(0xffffffffu, hi[c], 1);
+        } else {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            uL[c] = RG(sB, c, tx);
+            uR[c] = RG(sB, c, tx + 1);
+          }
+        }
+        if constexpr (NI == 1) {
+          auto cells = [&](double* a, double* b) {  // fallback only: loaded on demand
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              a[c] = RG(sB, c, tx);
+              b[c] = RG(sB, c, tx + 1);
+            }
+          };
+          unsigned eb = 0;
+          interface_flux_lazy<EQ, FLUX, DIM, RECON>(uL, uR, cells, 0, p.P, Gx, eb);
+          if (eb && tx >= 1 && xf <= p.n[0]) errb |= 1u;
+        } else {
+#pragma unroll
+          for (int i = 0; i < NI; ++i) {
+            unsigned eb = 0;
+            interface_flux<EQ, FLUX, DIM, RECON>(uL + i, uR + i, uL + i, uR + i, 0, p.P, Gx + i, eb);
+            if (eb && tx >= 1 && xf <= p.n[0]) errbs[i] |= 1u;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const double Gr = __shfl_down_sync(0xffffffffu, Gx[c], 1);  // lane 31's is unused
+#if FVB_FAST
+          gx[c * NT + tx] = (Gx[c] - Gr) * p.id[0];
+#else
+          gx[c * NT + tx] = 0.0 - ddiv(Gr - Gx[c], p, 0);
+#endif
+        }
+      } else {
       if constexpr (WENO) {
         double um[NC], uc[NC], up[NC], hi[NC], lo[NC];
 #pragma unroll
@@ -1010,6 +1066,7 @@ ring_kernel(const StageParams p) {
         }
 #pragma unroll
         for (int c = 0; c < NC; ++c) gx[c * NT + tx] = Gx[c];
+      }
       }
       // the x residual of this row is read from gx by the next iteration's
       // finish, after that iteration's top barrier
