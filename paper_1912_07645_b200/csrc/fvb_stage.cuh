@@ -779,9 +779,10 @@ ring_kernel(const StageParams p) {
   constexpr int W = NT + 2;
   extern __shared__ double smem[];
   double* ring = smem;                               // [kRingRows][NC][W]
+  constexpr bool kFaceBuf = WENO && NT != 32;       // one-warp blocks exchange faces by shuffle
   double* hx = ring + kRingRows * NC * W;            // [NC][NT]
-  double* lx = hx + (WENO ? NC * NT : 0);            // [NC][NT]
-  double* gx = lx + (WENO ? NC * NT : 0);            // [NC][NT]
+  double* lx = hx + (kFaceBuf ? NC * NT : 0);        // [NC][NT]
+  double* gx = lx + (kFaceBuf ? NC * NT : 0);        // [NC][NT]
   double* nring = gx + NC * NT;                      // [3][NC][NT]: u^n rows for the RK combination
   // march recurrence (high face H and flux G of the previous row) lives in
   // shared memory, not registers: it is idle during the whole x sweep
@@ -1100,8 +1101,8 @@ ring_kernel(const StageParams p) {
 template <int EQ, int RECON, int NT, int NI = 1>
 constexpr int ring_smem_bytes() {
   constexpr int NC = NComp<EQ, 2>::value * NI;
-  return 8 * (kRingRows * NC * (NT + 2) + (RECON != RECON_NONE ? 2 : 0) * NC * NT + NC * NT + 3 * NC * NT +
-              2 * NC * NT);
+  return 8 * (kRingRows * NC * (NT + 2) + (RECON != RECON_NONE && NT != 32 ? 2 : 0) * NC * NT + NC * NT +
+              3 * NC * NT + 2 * NC * NT);
 }
 
 // ---------------------------------------------------------------------------
