@@ -23,7 +23,7 @@ constexpr int kStripWarps = 4;
 #define FVB_RING_NT_SCALAR 32
 #endif
 // Euler: two-warp blocks; scalar laws: one-warp blocks whose x sweep runs on
-// shuffles (measured: Euler 19.2 vs 15.5 at 32, Burgers 107.5 vs 114 at 32)
+// shuffles (measured: Euler 19.3 at 64 vs 19.0 at 32; Burgers 107.5 vs 114)
 constexpr int kRingNT = FVB_RING_NT, kRingNTScalar = FVB_RING_NT_SCALAR;
 
 // cells per block along x (reported as nt-2) and the y tile (nty-2, 3D only)
