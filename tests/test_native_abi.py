@@ -25,6 +25,10 @@ def test_header_declares_what_ctypes_binds():
 def test_library_exports_every_symbol():
     from paper_1912_07645_b200 import _native as N
 
+    if not N.LIB_PATH.exists():  # fresh checkout: build it (nvcc cross-compiles, no GPU needed)
+        from paper_1912_07645_b200 import build as B
+
+        B.build()
     lib = N.load_library()
     for name in _declared():
         assert hasattr(lib, name), name
