@@ -37,6 +37,28 @@ void stage_block(int dim, int eq, int variant, int& nt, int& nty) {
   else { nt = Blk<3>::NT; nty = Blk<3>::NTY; }
 }
 
+// Launch with programmatic stream serialisation (the kernel waits on
+// griddepcontrol before its first dependent read), so a stage's CTAs are
+// scheduled while the previous stage's last blocks drain.
+template <typename K>
+static void launch_pdl(K kern, dim3 grid, dim3 block, int smem, cudaStream_t s, const StageParams& p) {
+#if FVB_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, p);
+#else
+  kern<<<grid, block, smem, s>>>(p);
+#endif
+}
+
 // opt a kernel into more than 48 KB of dynamic shared memory, once per device
 template <typename K>
 static void ensure_smem(K kern, int smem, unsigned& done_mask) {
@@ -67,17 +89,17 @@ static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
       if constexpr (NComp<EQ, 2>::value == 1) {
         if (p.ni == 2) {  // two instances per block (batched scalar ensembles)
           const int smem = ring_smem_bytes<EQ, RECON, NT, 2>() + 8 * (p.H + kRingPD + 4);
-          ring_kernel<EQ, FLUX, RECON, NT, FIN, 2><<<grid, NT, smem, s>>>(p);
+          launch_pdl(ring_kernel<EQ, FLUX, RECON, NT, FIN, 2>, grid, dim3(NT), smem, s, p);
           return 0;
         }
         if (p.ni == 4) {
           const int smem = ring_smem_bytes<EQ, RECON, NT, 4>() + 8 * (p.H + kRingPD + 4);
-          ring_kernel<EQ, FLUX, RECON, NT, FIN, 4><<<grid, NT, smem, s>>>(p);
+          launch_pdl(ring_kernel<EQ, FLUX, RECON, NT, FIN, 4>, grid, dim3(NT), smem, s, p);
           return 0;
         }
       }
       const int smem = ring_smem_bytes<EQ, RECON, NT>() + 8 * (p.H + kRingPD + 4);  // + row-offset table
-      ring_kernel<EQ, FLUX, RECON, NT, FIN><<<grid, NT, smem, s>>>(p);
+      launch_pdl(ring_kernel<EQ, FLUX, RECON, NT, FIN>, grid, dim3(NT), smem, s, p);
       return 0;
     }
   }

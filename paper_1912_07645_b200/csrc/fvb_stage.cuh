@@ -755,6 +755,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+#ifndef FVB_PDL
+#define FVB_PDL 1
+#endif
 #ifndef FVB_RING_MINB
 #define FVB_RING_MINB (512 / NT)  // 16 warps/SM at 128 registers
 #endif
@@ -791,6 +794,11 @@ ring_kernel(const StageParams p) {
   auto RG = [&](int slot, int c, int x) -> double& { return ring[(slot * NC + c) * W + x]; };
   auto NR = [&](int slot, int c) -> double& { return nring[(slot * NC + c) * NT + threadIdx.x]; };
 
+#if FVB_PDL
+  // programmatic dependent launch: this grid may be scheduled while the
+  // previous stage drains; nothing it reads is touched before the wait
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#endif
   const int inst = blockIdx.z * NI;
   FvbState* st = p.st + (p.shared_state ? 0 : inst);
   FvbState* sts[NI];
@@ -1075,6 +1083,9 @@ ring_kernel(const StageParams p) {
     sA = sB;
   }
   cp_async_wait<0>();
+#if FVB_PDL
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // this block's stage work is done
+#endif
   if constexpr (NI == 1) {
     if (errb) {
 #pragma unroll
