@@ -362,8 +362,12 @@ def cpu_reference_step(pool, u_pad, n, workers, shm_in, shm_out):
     return O.padded_from_interior(sc, O.rk_combine(O.interior(u_pad, sc).copy(), dt, Lfun, 3))
 
 
-def bench_cpu(n, steps, workers):
-    """Returns (Gcell-stage/s, seconds per step) of the oracle on the host."""
+def bench_cpu(n, steps, workers, warmup=1, budget_s=180.0):
+    """Returns (Gcell-stage/s, seconds per step, steps timed) of the oracle on the host.
+
+    ``warmup`` untimed steps, then up to ``steps`` timed RK3 steps; the timed
+    loop stops early once ``budget_s`` seconds are spent (a bounded sample
+    on slow hosts), and the number of steps actually timed is returned."""
     import multiprocessing as mp
     from multiprocessing import shared_memory
 
@@ -375,17 +379,23 @@ def bench_cpu(n, steps, workers):
     ctx = mp.get_context("fork")
     try:
         with ctx.Pool(workers) as pool:
-            cur = cpu_reference_step(pool, u, n, workers, shm_in, shm_out)  # warm the pool
-            tic = time.perf_counter()
-            for _ in range(steps):
+            cur = u
+            for _ in range(max(1, warmup)):  # warm the pool (untimed)
                 cur = cpu_reference_step(pool, cur, n, workers, shm_in, shm_out)
+            done = 0
+            tic = time.perf_counter()
+            while done < steps:
+                cur = cpu_reference_step(pool, cur, n, workers, shm_in, shm_out)
+                done += 1
+                if time.perf_counter() - tic > budget_s:
+                    break
             el = time.perf_counter() - tic
     finally:
         shm_in.close()
         shm_in.unlink()
         shm_out.close()
         shm_out.unlink()
-    return n * n * 3 * steps / el / 1e9, el / steps
+    return n * n * 3 * done / el / 1e9, el / done, done
 
 
 def main():
@@ -432,15 +442,17 @@ def main():
         if rank != 0:
             return
         workers = max(1, cores)
-        val, sps = bench_cpu(args.cells, max(1, args.cpu_steps), workers)
+        # the driver's --steps K --warmup W: W untimed full RK3 steps, then K
+        # timed ones (cut short after 180 s on a slow host; "steps" says how many)
+        val, sps, done = bench_cpu(args.cells, max(1, args.steps), workers, warmup=max(1, args.warmup))
         line = {
             "impl": "reference", "metric": METRIC, "value": round(val, 6), "unit": UNIT, "n_gpus": ws,
-            "steps": max(1, args.cpu_steps), "warmup": 1, "ms_per_step": round(sps * 1e3, 3),
+            "steps": done, "warmup": max(1, args.warmup), "ms_per_step": round(sps * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (KH2D preset, MC seed 42 sample 0)",
             "config": {"workload": workload, "arith": "numpy (reference op order)"},
             "cpu_baseline": {"value": round(val, 6), "unit": UNIT, "cores": workers, "kind": "port",
-                             "sample": f"{max(1, args.cpu_steps)} RK3 step(s) of KH2D {args.cells}^2 through the "
+                             "sample": f"{done} timed RK3 step(s) of KH2D {args.cells}^2 through the "
                                        f"numpy oracle, residual row-band split over {workers} processes"},
             "e2e": {"value": round(val, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }
@@ -454,7 +466,7 @@ def main():
     if not args.no_cpu and args.config == "kh2d":
         # bounded CPU sample: 1 RK3 step of the same workload, single process
         # (numpy is single threaded), the oracle = reference op order
-        val, sps = bench_cpu(args.cells, 1, 1)
+        val, sps, _ = bench_cpu(args.cells, max(1, args.cpu_steps), 1)
         cpu = {"value": round(val, 6), "unit": UNIT, "cores": 1, "kind": "port",
                "sample": f"1 RK3 step of KH2D {args.cells}^2 through the numpy oracle (oracle/fv_oracle.py), "
                          f"1 process, {sps:.1f} s"}

@@ -41,4 +41,5 @@ def test_bench_line_keys():
 def test_reference_arm_line():
     d = _run("--impl", "reference", "--steps", "1", "--warmup", "3")
     assert d["impl"] == "reference" and d["value"] > 0
+    assert d["steps"] == 1 and d["warmup"] == 3  # the driver's K and W are honoured
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["value"] == d["value"]
