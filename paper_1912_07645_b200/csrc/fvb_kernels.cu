@@ -42,6 +42,8 @@ void stage_block(int dim, int eq, int variant, int& nt, int& nty) {
 // scheduled while the previous stage's last blocks drain.
 template <typename K>
 static void launch_pdl(K kern, dim3 grid, dim3 block, int smem, cudaStream_t s, const StageParams& p) {
+  // wider ring blocks (-DFVB_RING_NT=96/128) need more than 48 KB
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 #if FVB_PDL
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
