@@ -761,7 +761,10 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #ifndef FVB_RING_MINB
 #define FVB_RING_MINB (512 / NT)  // 16 warps/SM at 128 registers
 #endif
-constexpr int kRingPD = 2;               // rows in flight ahead of the consumer
+#ifndef FVB_RING_PD
+#define FVB_RING_PD 1  // measured (profiles/r01_ring_pd_sweep.json): 1 row ahead +1 % over 2; 3-4 exceed the shared memory of 8 blocks/SM
+#endif
+constexpr int kRingPD = FVB_RING_PD;     // rows in flight ahead of the consumer
 constexpr int kRingRows = kRingPD + 3;   // ring slots
 
 // NI > 1 (scalar laws, batched ensembles): one block marches the same
