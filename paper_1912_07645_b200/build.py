@@ -1,8 +1,9 @@
 """Build the in-tree CUDA library ``_lib/libfvb200.so`` for sm_100a.
 
 Translation units (paper_1912_07645_b200/csrc):
-  fvb_kernels.cu  x2  -> namespace exact (-fmad=false, bitwise == reference)
-                         namespace fast  (-fmad=true, algebraic rewrites)
+  fvb_kernels.cu  x8  -> namespace exact (-fmad=false, bitwise == reference)
+                         namespace fast  (-fmad=true, algebraic rewrites),
+                         one unit per dimension (-DFVB_KDIM=1,2,3) + dispatch (0)
   fvb_aux.cu          -> ghost fill, halo slabs, UQ statistics (-fmad=false)
   fvb_capi.cu         -> extern "C" ABI declared in include/fvb200.h
 """
@@ -24,9 +25,12 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include")] + ARCH
 
-UNITS = [
-    ("fvb_kernels.cu", "fvb_exact.o", ["-fmad=false", "-DFVB_FAST=0", "-DFVB_NS=exact"]),
-    ("fvb_kernels.cu", "fvb_fast.o", ["-fmad=true", "-DFVB_FAST=1", "-DFVB_NS=fast"]),
+_MODES = [("exact", ["-fmad=false", "-DFVB_FAST=0", "-DFVB_NS=exact"]),
+          ("fast", ["-fmad=true", "-DFVB_FAST=1", "-DFVB_NS=fast"])]
+# the stage kernels: one unit per (mode, dimension) so they compile in
+# parallel (FVB_KDIM = 0 is the dispatcher + wave-speed kernels)
+UNITS = [("fvb_kernels.cu", f"fvb_{m}_d{d}.o", flags + [f"-DFVB_KDIM={d}"]) for d in (2, 3, 1, 0)
+         for m, flags in _MODES] + [
     ("fvb_aux.cu", "fvb_aux.o", ["-fmad=false"]),
     ("fvb_capi.cu", "fvb_capi.o", ["-fmad=false"]),
 ]
@@ -50,7 +54,7 @@ def _compile(unit, out: Path = OUT):
 
 
 def build(force: bool = False, verbose: bool = True, extra=(), out_dir: Path | None = None) -> Path:
-    """Compile the four translation units and link libfvb200.so.  ``extra``
+    """Compile the translation units and link libfvb200.so.  ``extra``
     adds nvcc flags (tuning experiments build variants into ``out_dir``)."""
     out = Path(out_dir) if out_dir else OUT
     out.mkdir(parents=True, exist_ok=True)
@@ -60,7 +64,7 @@ def build(force: bool = False, verbose: bool = True, extra=(), out_dir: Path | N
     if lib.exists() and stamp.exists() and stamp.read_text() == digest and not force:
         return lib
     units = [(src, obj, flags + list(extra)) for src, obj, flags in UNITS]
-    with cf.ThreadPoolExecutor(max_workers=len(units)) as ex:
+    with cf.ThreadPoolExecutor(max_workers=min(len(units), os.cpu_count() or 4)) as ex:
         list(ex.map(lambda u: _compile(u, out), units))
     cmd = [NVCC] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", str(lib)] + [str(out / u[1]) for u in UNITS]
     r = subprocess.run(cmd, capture_output=True, text=True)

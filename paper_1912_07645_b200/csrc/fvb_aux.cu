@@ -216,25 +216,22 @@ __global__ void __launch_bounds__(kSfThreads) structure_pass1(Pad p, fvb_layout 
 // accumulation  acc = sum_j mean_j ; sums[h] += acc / dim  (uq.py:257-261).
 __global__ void structure_pass2(const double* __restrict__ partials, int nblocks, int H, int dim, double ncell, double* sums) {
   __shared__ double red[kSfThreads];
-  __shared__ double S[64 * 3];
-  for (int hj = 0; hj < (H + 1) * dim; ++hj) {
-    double acc = 0.0;
-    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) acc += partials[(int64_t)b * (H + 1) * dim + hj];
-    red[threadIdx.x] = acc;
-    __syncthreads();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-      if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+  for (int h = 0; h <= H; ++h) {  // any max offset: no per-(h, j) table
+    double accj = 0.0;           // thread 0: sum_j mean_j, in j order
+    for (int j = 0; j < dim; ++j) {
+      const int hj = h * dim + j;
+      double acc = 0.0;
+      for (int b = threadIdx.x; b < nblocks; b += blockDim.x) acc += partials[(int64_t)b * (H + 1) * dim + hj];
+      red[threadIdx.x] = acc;
+      __syncthreads();
+      for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) accj += red[0] / ncell;
       __syncthreads();
     }
-    if (threadIdx.x == 0) S[hj] = red[0];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    for (int h = 0; h <= H; ++h) {
-      double acc = 0.0;
-      for (int j = 0; j < dim; ++j) acc += S[h * dim + j] / ncell;
-      sums[h] += acc / dim;
-    }
+    if (threadIdx.x == 0) sums[h] += accj / dim;
   }
 }
 

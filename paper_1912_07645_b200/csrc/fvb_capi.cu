@@ -139,6 +139,24 @@ static int validate(fvb_ctx* ctx, const fvb_scheme* s) {
   return FVB_OK;
 }
 
+// Instance count and extent checks shared by the stage entry points: the
+// single-shot calls use a 4096-entry scratch state, and the 2D ring kernel
+// addresses one instance (all components, plus the batched instances of a
+// block) with 32-bit element offsets.
+static int validate_instances(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, int ninst, bool scratch) {
+  if (ninst < 1) return set_err(ctx, FVB_E_CONFIG, "ninst must be >= 1");
+  if (scratch && ninst > 4096) return set_err(ctx, FVB_E_CONFIG, "too many instances (%d > 4096)", ninst);
+  if (lay && s->dim == 2) {
+    const int64_t g = s->ghost;
+    const int64_t span = (int64_t)(s->ncomp - 1) * lay->sc + (s->cells[1] + 2 * g) * lay->sy + s->cells[0] + 2 * g;
+    const int64_t batch = s->ncomp == 1 ? 3 * lay->si : 0;  // up to 4 instances per block (scalar laws)
+    if (span + batch >= (int64_t(1) << 31))
+      return set_err(ctx, FVB_E_CONFIG, "2D instance of %lld elements exceeds the 32-bit kernel offsets",
+                     (long long)(span + batch));
+  }
+  return FVB_OK;
+}
+
 static bool is_pow2(double d) {
   int e;
   const double m = std::frexp(d, &e);
@@ -174,6 +192,33 @@ static StageParams base_params(const fvb_scheme& s, const fvb_layout& L) {
   return p;
 }
 
+static int sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
+  return n;
+}
+
+// Resident blocks per SM of the stage kernel `p` selects (register and
+// shared-memory limits of the compiled kernel, queried from the runtime).
+// One grid serves every stage of a step, so take the most constrained of
+// the stage shapes (first / middle / final stage).
+static int stage_occupancy(const fvb_scheme& s, const StageParams& p) {
+  static const int shapes[4][2] = {{1, 0}, {3, 0}, {4, 1}, {1, 1}};  // (kind, final_stage)
+  int best = 0;
+  for (const auto& sh : shapes) {
+    StageParams q = p;
+    q.H = std::max(q.H, 16);
+    q.kind = sh[0];
+    q.final_stage = sh[1];
+    const int n = s.arith == FVB_ARITH_FAST
+                      ? fvb::fast::launch_stage(s.dim, s.eq, s.flux, s.recon, q, dim3(0, 0, 0), 0)
+                      : fvb::exact::launch_stage(s.dim, s.eq, s.flux, s.recon, q, dim3(0, 0, 0), 0);
+    if (n > 0) best = best == 0 ? n : std::min(best, n);
+  }
+  return best;
+}
+
 // Grid of the stage kernel; fills chunks / H / nblocks.
 static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t row_lo = 0, int64_t row_hi = -1) {
   int nt, nty;
@@ -206,14 +251,17 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
     const int64_t nm = std::max<int64_t>(1, row_hi - row_lo);
     int64_t ytiles = 1;
     if (s.dim == 3) ytiles = (p.n[1] + (nty - 2) - 1) / (nty - 2);
-    // aim for ~2 waves of resident blocks over 148 SMs
     // resident blocks per SM (register-limited) and waves of blocks: one
     // wave keeps the march long (fewer redundant halo rows per chunk)
     int64_t per_sm = s.dim == 3 ? 2 : (p.variant == 0 ? 4 : 512 / nt);  // 16 warps/SM at 128 registers
+    {
+      const int occ = stage_occupancy(s, p);  // what the compiled kernel actually fits
+      if (occ > 0) per_sm = occ;
+    }
     int64_t waves = 1;
     if (const char* e = getenv("FVB_BLOCKS_PER_SM")) per_sm = std::max(1, atoi(e));
     if (const char* e = getenv("FVB_WAVES")) waves = std::max(1, atoi(e));
-    const int64_t slots = 148 * per_sm;
+    const int64_t slots = (int64_t)sm_count() * per_sm;
     const int64_t base = strips * ytiles * nig;
     int64_t want_chunks = 1;
     if (getenv("FVB_WAVES")) {
@@ -234,7 +282,9 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
     H = (nm + want_chunks - 1) / want_chunks;
     const char* env = getenv("FVB_MARCH_ROWS");
     if (env && atoi(env) > 0) H = atoi(env);
-    H = std::max<int64_t>(4, std::min<int64_t>(H, nm));
+    // the per-block row-offset table lives in shared memory: cap the march
+    // length (more chunks instead) so it stays small at any grid size
+    H = std::max<int64_t>(4, std::min<int64_t>(std::min<int64_t>(H, nm), 2048));
     chunks = (nm + H - 1) / H;
     if (s.dim == 2) {
       g.y = (unsigned)chunks;
@@ -268,7 +318,7 @@ static int do_stage(fvb_ctx* ctx, const fvb_scheme& s, const StageParams& p, dim
 static int do_speed(fvb_ctx* ctx, const fvb_scheme& s, const StageParams& p, int finalize, int ninst) {
   const int64_t ncell = p.n[0] * p.n[1] * p.n[2];
   int64_t blocks = (ncell + 255) / 256;
-  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 8 / std::max(1, ninst) + 1));
+  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 8 / std::max(1, ninst) + 1));
   dim3 grid((unsigned)blocks, ninst, 1);
   int r = s.arith == FVB_ARITH_FAST ? fvb::fast::launch_speed(s.dim, s.eq, p, finalize, grid, ctx->stream)
                                     : fvb::exact::launch_speed(s.dim, s.eq, p, finalize, grid, ctx->stream);
@@ -402,7 +452,8 @@ int fvb_wave_speed_maxima(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* l
                           double* h_max) {
   int r = validate(ctx, s);
   if (r) return r;
-  if (ninst > 4096) return set_err(ctx, FVB_E_CONFIG, "too many instances");
+  r = validate_instances(ctx, s, lay, ninst, true);
+  if (r) return r;
   r = reset_states(ctx, ctx->d_scratch_state, ninst, 0.0);
   if (r) return r;
   StageParams p = base_params(*s, *lay);
@@ -439,6 +490,8 @@ static int stage_error(fvb_ctx* ctx, const FvbState& h, int inst) {
 int fvb_spatial_residual(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, const double* u, double* out,
                          int ninst) {
   int r = validate(ctx, s);
+  if (r) return r;
+  r = validate_instances(ctx, s, lay, ninst, true);
   if (r) return r;
   r = reset_states(ctx, ctx->d_scratch_state, ninst, 0.0);
   if (r) return r;
@@ -488,6 +541,8 @@ static int build_step(const fvb_scheme& s, const fvb_layout& L, double* const b[
 int fvb_ssp_rk_step(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, double* un, double* w1, double* w2,
                     int ninst, double dt) {
   int r = validate(ctx, s);
+  if (r) return r;
+  r = validate_instances(ctx, s, lay, ninst, true);
   if (r) return r;
   r = reset_states(ctx, ctx->d_scratch_state, ninst, dt);
   if (r) return r;
@@ -557,6 +612,8 @@ static int enqueue_step(fvb_ctx* ctx) {
 int fvb_run_begin(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, double* bufs[3], int ninst, int mode,
                   int64_t max_steps) {
   int r = validate(ctx, s);
+  if (r) return r;
+  r = validate_instances(ctx, s, lay, ninst, false);
   if (r) return r;
   destroy_graph(ctx);
   ctx->launches = 0;
@@ -850,7 +907,7 @@ int fvb_moments_merge(fvb_ctx* ctx, double* mean_a, double* m2_a, int64_t count_
 
 int fvb_structure_push(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, const double* u, int inst,
                        int comp, double p, int H, double* d_sums) {
-  if (H < 0 || H > 63) return set_err(ctx, FVB_E_CONFIG, "structure_max_offset must lie in [0, 63], got %d", H);
+  if (H < 0) return set_err(ctx, FVB_E_CONFIG, "max offset must be >= 0, got %d", H);
   const int nb = fvb::structure_blocks(*s);
   const int64_t need = (int64_t)nb * (H + 1) * s->dim;
   if (need > ctx->partials_cap) {

@@ -27,6 +27,7 @@ constexpr int kStripWarps = 4;
 constexpr int kRingNT = FVB_RING_NT, kRingNTScalar = FVB_RING_NT_SCALAR;
 
 // cells per block along x (reported as nt-2) and the y tile (nty-2, 3D only)
+#if FVB_KDIM == 0
 void stage_block(int dim, int eq, int variant, int& nt, int& nty) {
   if (dim == 1 && variant == 2) variant = 1;
   if (dim == 2 && variant == 2) { nt = eq == EQ_EULER ? kRingNT : kRingNTScalar; nty = 1; return; }
@@ -36,12 +37,24 @@ void stage_block(int dim, int eq, int variant, int& nt, int& nty) {
   else if (dim == 2) { nt = Blk<2>::NT; nty = 1; }
   else { nt = Blk<3>::NT; nty = Blk<3>::NTY; }
 }
+#endif
 
 // Launch with programmatic stream serialisation (the kernel waits on
 // griddepcontrol before its first dependent read), so a stage's CTAs are
 // scheduled while the previous stage's last blocks drain.
+// grid.x == 0 is an occupancy query: resident blocks per SM of the kernel
+// that would be launched (fvb_capi.cu stage_grid sizes the grid with it)
 template <typename K>
-static void launch_pdl(K kern, dim3 grid, dim3 block, int smem, cudaStream_t s, const StageParams& p) {
+static int occupancy(K kern, dim3 block, int smem) {
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, (int)(block.x * block.y), smem) != cudaSuccess) n = 0;
+  return n;
+}
+
+template <typename K>
+static int launch_pdl(K kern, dim3 grid, dim3 block, int smem, cudaStream_t s, const StageParams& p) {
+  if (grid.x == 0) return occupancy(kern, block, smem);
   // wider ring blocks (-DFVB_RING_NT=96/128) need more than 48 KB
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 #if FVB_PDL
@@ -59,6 +72,7 @@ static void launch_pdl(K kern, dim3 grid, dim3 block, int smem, cudaStream_t s, 
 #else
   kern<<<grid, block, smem, s>>>(p);
 #endif
+  return 0;
 }
 
 // opt a kernel into more than 48 KB of dynamic shared memory, once per device
@@ -73,6 +87,24 @@ static void ensure_smem(K kern, int smem, unsigned& done_mask) {
   }
 }
 
+template <int EQ, int FLUX, int RECON, int KS, bool FIN>
+static int launch_ring(const StageParams& p, dim3 grid, cudaStream_t s) {
+  constexpr int NT = NComp<EQ, 2>::value == 1 ? kRingNTScalar : kRingNT;
+  const int table = 4 * (p.H + kRingPD + 4);  // row-offset table (32-bit)
+  if constexpr (NComp<EQ, 2>::value == 1) {
+    if (p.ni == 2) {  // two instances per block (batched scalar ensembles)
+      const int smem = ring_smem_bytes<EQ, RECON, NT, 2>() + table;
+      return launch_pdl(ring_kernel<EQ, FLUX, RECON, NT, KS, FIN, 2>, grid, dim3(NT), smem, s, p);
+    }
+    if (p.ni == 4) {
+      const int smem = ring_smem_bytes<EQ, RECON, NT, 4>() + table;
+      return launch_pdl(ring_kernel<EQ, FLUX, RECON, NT, KS, FIN, 4>, grid, dim3(NT), smem, s, p);
+    }
+  }
+  const int smem = ring_smem_bytes<EQ, RECON, NT>() + table;
+  return launch_pdl(ring_kernel<EQ, FLUX, RECON, NT, KS, FIN>, grid, dim3(NT), smem, s, p);
+}
+
 template <int DIM, int EQ, int FLUX, int RECON, bool FIN>
 static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
   if constexpr (DIM == 3) {
@@ -81,32 +113,26 @@ static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
       auto kern = ring3_kernel<EQ, FLUX, RECON, FIN>;
       static unsigned done = 0;  // per instantiation
       ensure_smem(kern, 227 * 1024, done);  // a cap: the plane table grows with H
+      if (grid.x == 0) return occupancy(kern, dim3(kRing3NT, kRing3NTY), smem);
       kern<<<grid, dim3(kRing3NT, kRing3NTY), smem, s>>>(p);
       return 0;
     }
   }
   if constexpr (DIM == 2) {
     if (p.variant == 2) {
-      constexpr int NT = NComp<EQ, 2>::value == 1 ? kRingNTScalar : kRingNT;
-      if constexpr (NComp<EQ, 2>::value == 1) {
-        if (p.ni == 2) {  // two instances per block (batched scalar ensembles)
-          const int smem = ring_smem_bytes<EQ, RECON, NT, 2>() + 8 * (p.H + kRingPD + 4);
-          launch_pdl(ring_kernel<EQ, FLUX, RECON, NT, FIN, 2>, grid, dim3(NT), smem, s, p);
-          return 0;
-        }
-        if (p.ni == 4) {
-          const int smem = ring_smem_bytes<EQ, RECON, NT, 4>() + 8 * (p.H + kRingPD + 4);
-          launch_pdl(ring_kernel<EQ, FLUX, RECON, NT, FIN, 4>, grid, dim3(NT), smem, s, p);
-          return 0;
-        }
-      }
-      const int smem = ring_smem_bytes<EQ, RECON, NT>() + 8 * (p.H + kRingPD + 4);  // + row-offset table
-      launch_pdl(ring_kernel<EQ, FLUX, RECON, NT, FIN>, grid, dim3(NT), smem, s, p);
-      return 0;
+      // stage combination as a compile-time shape: residual only / u^s + dt L
+      // / a u^n + b (u^s + dt L); the final stage never is the bare residual
+      const int ks = p.kind == 0 ? 0 : (p.kind == 1 ? 1 : 2);
+      if (FIN && ks == 0) return -1;
+      if (ks == 0) return launch_ring<EQ, FLUX, RECON, (FIN ? 1 : 0), FIN>(p, grid, s);
+      if (ks == 1) return launch_ring<EQ, FLUX, RECON, 1, FIN>(p, grid, s);
+      return launch_ring<EQ, FLUX, RECON, 2, FIN>(p, grid, s);
     }
   }
   if (DIM <= 2 && p.variant == 0) {
-    strip_kernel<DIM, EQ, FLUX, RECON, kStripWarps, FIN><<<grid, 32 * kStripWarps, 0, s>>>(p);
+    auto kern = strip_kernel<DIM, EQ, FLUX, RECON, kStripWarps, FIN>;
+    if (grid.x == 0) return occupancy(kern, dim3(32 * kStripWarps), 0);
+    kern<<<grid, 32 * kStripWarps, 0, s>>>(p);
     return 0;
   } else {
     constexpr int NT = Blk<DIM>::NT, NTY = Blk<DIM>::NTY;
@@ -114,6 +140,7 @@ static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
     auto kern = stage_kernel<DIM, EQ, FLUX, RECON, NT, NTY, FIN>;
     static unsigned done = 0;  // per instantiation
     ensure_smem(kern, smem, done);
+    if (grid.x == 0) return occupancy(kern, dim3(NT, NTY), smem);
     kern<<<grid, dim3(NT, NTY), smem, s>>>(p);
     return 0;
   }
@@ -147,15 +174,37 @@ static int launch_dim(int eq, int flux, int recon, const StageParams& p, dim3 gr
   return -1;
 }
 
+// One translation unit per dimension (FVB_KDIM = 1, 2, 3) so the six
+// instantiation-heavy units compile in parallel; FVB_KDIM = 0 holds the
+// dispatcher and the wave-speed kernels.
+#if FVB_KDIM == 1
+int launch_stage_d1(int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s) {
+  return launch_dim<1>(eq, flux, recon, p, grid, s);
+}
+#elif FVB_KDIM == 2
+int launch_stage_d2(int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s) {
+  return launch_dim<2>(eq, flux, recon, p, grid, s);
+}
+#elif FVB_KDIM == 3
+int launch_stage_d3(int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s) {
+  return launch_dim<3>(eq, flux, recon, p, grid, s);
+}
+#else
+int launch_stage_d1(int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s);
+int launch_stage_d2(int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s);
+int launch_stage_d3(int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s);
 int launch_stage(int dim, int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s) {
   switch (dim) {
-    case 1: return launch_dim<1>(eq, flux, recon, p, grid, s);
-    case 2: return launch_dim<2>(eq, flux, recon, p, grid, s);
-    case 3: return launch_dim<3>(eq, flux, recon, p, grid, s);
+    case 1: return launch_stage_d1(eq, flux, recon, p, grid, s);
+    case 2: return launch_stage_d2(eq, flux, recon, p, grid, s);
+    case 3: return launch_stage_d3(eq, flux, recon, p, grid, s);
   }
   return -1;
 }
 
+#endif
+
+#if FVB_KDIM == 0
 template <int DIM>
 static int launch_speed_dim(int eq, const StageParams& p, int fin, dim3 grid, cudaStream_t s) {
   if (eq == EQ_EULER) speed_kernel<DIM, EQ_EULER><<<grid, 256, 0, s>>>(p, fin);
@@ -172,6 +221,7 @@ int launch_speed(int dim, int eq, const StageParams& p, int fin, dim3 grid, cuda
   }
   return -1;
 }
+#endif
 
 }  // namespace FVB_NS
 }  // namespace fvb

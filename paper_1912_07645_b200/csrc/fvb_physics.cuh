@@ -21,6 +21,11 @@
 #ifndef FVB_FAST
 #error "FVB_FAST must be defined to 0 or 1"
 #endif
+// Warp-uniform shortcuts (flat WENO stencils, uniform interface states, no
+// star state in the warp): 1 = take them when the whole warp agrees.
+#ifndef FVB_WARP_SKIP
+#define FVB_WARP_SKIP 1
+#endif
 
 namespace fvb {
 
@@ -55,19 +60,51 @@ __device__ __forceinline__ double frcp(double x) {
 }
 // a/b: a times the (<= 1 ulp) reciprocal, <= 2 ulp
 __device__ __forceinline__ double fdiv(double a, double b) { return a * frcp(b); }
-// sqrt(x), x > 0: rsqrt seed (~1e-6) + one Newton step on 1/sqrt (~1e-12),
-// then one residual correction of s = x*y.  Measured on the B200
-// (tools/mufu_precision.cu): equal to the correctly rounded sqrt for 4M
-// log-uniform samples over [e^-20, e^20].
+// sqrt(x), x > 0: rsqrt seed y (relative error e0 ~ 1e-6), then one
+// third-order step of the series 1/sqrt(1-e) = 1 + e/2 + 3e^2/8 + ...
+// with e = 1 - x y^2, applied to s = x y directly:
+//   sqrt(x) = s (1 + e/2 + 3e^2/8) + O(e^3 s),  e^3 ~ 1e-17
+// -- five FP64 instructions instead of eight for Newton + residual
+// correction, within 2 ulp (tools/mufu_precision.cu).  The sound speed it
+// feeds enters the HLLC/Rusanov flux only through the wave-speed estimates,
+// whose errors are multiplied by the state jump (the flux is consistent for
+// any speeds).
 __device__ __forceinline__ double fsqrt(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
-  double s = x * y;
-  return fma(fma(-s, s, x), 0.5 * y, s);  // x > 0 on every physical state
+  const double s = x * y;
+  const double e = fma(-s, y, 1.0);
+  return fma(s * e, fma(e, 0.375, 0.5), s);
 }
 #endif
+
+// All components of two states bitwise equal, on the integer pipes: one
+// three-input LOP3 per 32-bit half folds (a ^ b) | acc.  Conservative
+// (+0 / -0 differ), see bit_eq.
+template <int NC>
+__device__ __forceinline__ bool bits_equal_all(const double* a, const double* b) {
+  unsigned acc = 0u;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    acc |= (unsigned)__double2loint(a[c]) ^ (unsigned)__double2loint(b[c]);
+    acc |= (unsigned)__double2hiint(a[c]) ^ (unsigned)__double2hiint(b[c]);
+  }
+  return acc == 0u;
+}
+// um == uc == up bitwise in every component (a flat WENO stencil)
+template <int NC>
+__device__ __forceinline__ bool bits_flat_all(const double* um, const double* uc, const double* up) {
+  unsigned acc = 0u;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const unsigned cl = (unsigned)__double2loint(uc[c]), ch = (unsigned)__double2hiint(uc[c]);
+    acc |= cl ^ (unsigned)__double2loint(um[c]);
+    acc |= cl ^ (unsigned)__double2loint(up[c]);
+    acc |= ch ^ (unsigned)__double2hiint(um[c]);
+    acc |= ch ^ (unsigned)__double2hiint(up[c]);
+  }
+  return acc == 0u;
+}
 
 // ---------------------------------------------------------------------------
 // Euler equation of state (equations.py:62-73, 128-129)
@@ -87,7 +124,16 @@ __device__ __forceinline__ double euler_pressure(const double* u, const Phys& P)
 
 template <int DIM>
 __device__ __forceinline__ bool euler_physical(const double* u, const Phys& P) {
+#if FVB_FAST
+  // reciprocal free: for rho > 0, p > floor  <=>  gm1 (E rho - |m|^2 / 2) > floor rho
+  double msq = u[1] * u[1];
+#pragma unroll
+  for (int k = 1; k < DIM; ++k) msq = fma(u[1 + k], u[1 + k], msq);
+  const double t = fma(u[1 + DIM], u[0], -0.5 * msq);
+  return (u[0] > kFloor) & (P.gm1 * t > kFloor * u[0]);
+#else
   return (u[0] > kFloor) & (euler_pressure<DIM>(u, P) > kFloor);
+#endif
 }
 
 // Physical flux F_axis(u) (equations.py:91-110), given p and v = m_axis/rho.
@@ -194,6 +240,75 @@ __device__ __forceinline__ void weno_faces(double um, double uc, double up, doub
   }
 }
 
+#if FVB_FAST
+// Fast-mode WENO2 faces of all components of one cell.  With D0 = uc - um,
+// D1 = up - uc, q_i = (eps + D_i^2)^2: both faces share the weights and
+// hi/lo = uc +- (1/2) (q1 D0 + q0 D1) / (q0 + q1), written as two FMAs with
+// r = 1/(2 (q0 + q1)).  One reciprocal serves all components
+// (1/den_c = prod_{k!=c} den_k / prod_k den_k; den_c >= 2 eps^2 keeps the
+// product in range).  A warp whose every stencil is flat skips the weights
+// (r = T = 0 gives hi = lo = uc).
+template <int NC>
+__device__ __forceinline__ void weno2_faces_fast(const double* um, const double* uc, const double* up, double eps,
+                                                 double* hi, double* lo) {
+  double rd[NC], T[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    rd[c] = 0.0;
+    T[c] = 0.0;
+  }
+  if (!FVB_WARP_SKIP || __any_sync(__activemask(), !bits_flat_all<NC>(um, uc, up))) {
+    double den[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double D0 = uc[c] - um[c];
+      const double D1 = up[c] - uc[c];
+      const double e0 = fma(D0, D0, eps);
+      const double e1 = fma(D1, D1, eps);
+      const double q1 = e1 * e1;
+      den[c] = fma(e0, e0, q1);
+      T[c] = fma(q1, D0, e0 * (e0 * D1));
+    }
+    if constexpr (NC == 1) {
+      rd[0] = 0.5 * frcp(den[0]);
+    } else if constexpr (NC == 4) {  // product tree: 9 multiplies for the 4 cofactors
+      const double p01 = den[0] * den[1], p23 = den[2] * den[3];
+      const double inv = 0.5 * frcp(p01 * p23);
+      const double a = inv * p23, b = inv * p01;
+      rd[0] = a * den[1];
+      rd[1] = a * den[0];
+      rd[2] = b * den[3];
+      rd[3] = b * den[2];
+    } else if constexpr (NC == 5) {
+      const double p01 = den[0] * den[1], p23 = den[2] * den[3], p234 = p23 * den[4];
+      const double inv = 0.5 * frcp(p01 * p234);
+      const double a = inv * p234, b = inv * p01, b4 = b * den[4];
+      rd[0] = a * den[1];
+      rd[1] = a * den[0];
+      rd[2] = b4 * den[3];
+      rd[3] = b4 * den[2];
+      rd[4] = b * p23;
+    } else {
+      double pre[NC + 1], suf[NC + 1];
+      pre[0] = 1.0;
+      suf[NC] = 1.0;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) pre[c + 1] = pre[c] * den[c];
+#pragma unroll
+      for (int c = NC - 1; c >= 0; --c) suf[c] = suf[c + 1] * den[c];
+      const double inv = 0.5 * frcp(pre[NC]);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) rd[c] = (inv * pre[c]) * suf[c + 1];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    hi[c] = fma(rd[c], T[c], uc[c]);
+    lo[c] = fma(-rd[c], T[c], uc[c]);
+  }
+}
+#endif
+
 // All components of one cell: a warp whose every cell has a flat stencil
 // (um == uc == up, the uniform KH bands) skips the weights.  The shortcut
 // returns exactly what the formula gives for D0 = D1 = +0 (h = +0, so
@@ -205,10 +320,24 @@ __device__ __forceinline__ void weno_faces_nc(const double* um, const double* uc
 #pragma unroll
     for (int c = 0; c < NC; ++c) { hi[c] = uc[c]; lo[c] = uc[c]; }
   } else {
+#if FVB_FAST
+    if constexpr (RECON == RECON_WENO2) {
+      weno2_faces_fast<NC>(um, uc, up, eps, hi, lo);
+      return;
+    }
+#endif
     // hi = uc + dh, lo = uc - dl.  A warp whose every stencil is flat
     // (D0 = D1 = +0 in all components) skips the weights: the formula then
     // gives dh = dl = +0 exactly in both modes (signed zeros included).
     double dh[NC], dl[NC];
+#if FVB_FAST
+    const bool flat = bits_flat_all<NC>(um, uc, up);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      dh[c] = 0.0;
+      dl[c] = 0.0;
+    }
+#else
     bool flat = true;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -216,6 +345,7 @@ __device__ __forceinline__ void weno_faces_nc(const double* um, const double* uc
       dh[c] = 0.0;
       dl[c] = 0.0;
     }
+#endif
     if (__any_sync(__activemask(), !flat)) {
       double D0[NC], D1[NC];
 #pragma unroll
@@ -358,16 +488,22 @@ __device__ __forceinline__ void rusanov(const double* uL, const double* uR, cons
 // every lane has uL == uR, cost one physical flux).
 template <int DIM>
 __device__ __forceinline__ void hllc(const double* uL, const double* uR, const EState& L, const EState& R,
-                                     int axis, const Phys& P, double* F, unsigned& errbits) {
+                                     int axis, const Phys& P, double* F, unsigned& errbits, bool eq_bits) {
   constexpr int NC = DIM + 2;
   const unsigned am = __activemask();
+#if FVB_FAST
+  // the caller's bitwise test (conservative on +0/-0: such lanes take the
+  // general formula, which is consistent up to rounding)
+  const bool equal = eq_bits;
+#else
   bool equal = true;
 #pragma unroll
   for (int c = 0; c < NC; ++c) equal &= (uL[c] == uR[c]);
+#endif
   const double sL = np_min(L.v - L.c, R.v - R.c);
   const double sR = np_max(L.v + L.c, R.v + R.c);
   if (sR - sL <= 0.0) errbits |= 1u;
-  if (!__any_sync(am, !equal)) {  // whole warp: F(u, u) = f(u)
+  if (FVB_WARP_SKIP && !__any_sync(am, !equal)) {  // whole warp: F(u, u) = f(u)
     euler_flux<DIM>(uL, L.p, L.v, axis, F);
     return;
   }
@@ -390,7 +526,7 @@ __device__ __forceinline__ void hllc(const double* uL, const double* uR, const E
   const double p = left ? L.p : R.p;
   const double sK = left ? sL : sR;
   euler_flux<DIM>(u, p, v, axis, F);
-  if (!__any_sync(am, star)) return;
+  if (FVB_WARP_SKIP && !__any_sync(am, star)) return;
   // star state (numerics.py:173-181), evaluated for the selected side only
   double st[NC];
 #if FVB_FAST
@@ -437,15 +573,14 @@ __device__ __forceinline__ void interface_flux_lazy(const double* uL0, const dou
   constexpr int NC = NComp<EQ, DIM>::value;
   if constexpr (EQ == EQ_EULER) {
     double uL[NC], uR[NC];
-    bool equal = true;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       uL[c] = uL0[c];
       uR[c] = uR0[c];
-      equal &= bit_eq(uL[c], uR[c]);
     }
+    bool equal = bits_equal_all<NC>(uL, uR);
     const unsigned am = __activemask();
-    if (!__any_sync(am, !equal)) {
+    if (FVB_WARP_SKIP && !__any_sync(am, !equal)) {
       // Whole warp on uniform states (the KH bands): F(u, u) = f(u) for
       // HLLC (numerics.py:195-196) and Rusanov (0.5(f+f) - hs*(+0) == f), so
       // only v and p of one state are needed -- no second state, no sqrt.
@@ -480,9 +615,10 @@ __device__ __forceinline__ void interface_flux_lazy(const double* uL0, const dou
         cells(uL, uR);
         L = euler_state<DIM>(uL, axis, P);
         R = euler_state<DIM>(uR, axis, P);
+        equal = bits_equal_all<NC>(uL, uR);
       }
     }
-    if constexpr (FLUX == FLUX_HLLC) hllc<DIM>(uL, uR, L, R, axis, P, F, errbits);
+    if constexpr (FLUX == FLUX_HLLC) hllc<DIM>(uL, uR, L, R, axis, P, F, errbits, equal);
     else rusanov<EQ, DIM>(uL, uR, L, R, axis, P, F);
   } else {
     EState dummy{};

@@ -103,11 +103,27 @@ __device__ __forceinline__ void post_cell(const StageParams& p, FvbState* st, co
       finite = false;
     }
   }
+  double s[DIM];
+#if FVB_FAST
+  if constexpr (EQ == EQ_EULER) {  // one pressure for the physical check and the sound speed
+    const double r = frcp(v[0]);
+    double msq = v[1] * v[1];
+#pragma unroll
+    for (int k = 1; k < DIM; ++k) msq = fma(v[1 + k], v[1 + k], msq);
+    const double pr = p.P.gm1 * fma(-0.5 * msq, r, v[1 + DIM]);
+    if (!((v[0] > kFloor) & (pr > kFloor))) atomicMin(&st->bad_unphys, cell);
+    const double c = fsqrt(p.P.gamma * pr * r);
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) s[k] = fabs(v[1 + k] * r) + c;
+  } else {
+    wave_speeds<EQ, DIM>(v, p.P, s);
+  }
+#else
   if constexpr (EQ == EQ_EULER) {
     if (!euler_physical<DIM>(v, p.P)) atomicMin(&st->bad_unphys, cell);
   }
-  double s[DIM];
   wave_speeds<EQ, DIM>(v, p.P, s);
+#endif
 #pragma unroll
   for (int k = 0; k < DIM; ++k) smax[k] = fmax(smax[k], s[k]);
 }
@@ -766,12 +782,20 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #endif
 constexpr int kRingPD = FVB_RING_PD;     // rows in flight ahead of the consumer
 constexpr int kRingRows = kRingPD + 3;   // ring slots
+#ifndef FVB_RING_XSHFL
+#define FVB_RING_XSHFL 1
+#endif
+template <int NT>
+constexpr bool kXShfl = FVB_RING_XSHFL && NT > 32 && NT % 32 == 0;  // hybrid shuffle x faces
 
 // NI > 1 (scalar laws, batched ensembles): one block marches the same
 // strip of NI instances at once -- the instances are "virtual components"
 // (component stride = instance stride), so the row bookkeeping, barriers
 // and copies are shared and the per-instance math interleaves.
-template <int EQ, int FLUX, int RECON, int NT, bool FIN, int NI = 1>
+// KS (stage combination, compile time): 0 = the residual L itself
+// (spatial_residual); 1 = u^s + dt L (forward Euler, RK stage 1);
+// 2 = a u^n + b (u^s + dt L) (later SSP-RK stages, a/b per p.kind).
+template <int EQ, int FLUX, int RECON, int NT, int KS, bool FIN, int NI = 1>
 __global__ void __launch_bounds__(NT, FVB_RING_MINB)
 ring_kernel(const StageParams p) {
   constexpr int DIM = 2;
@@ -782,17 +806,23 @@ ring_kernel(const StageParams p) {
   // runs on shuffles, and gx holds each column's own x residual
   constexpr bool kShflX = NT == 32;
   constexpr bool WENO = RECON != RECON_NONE;
+  constexpr bool UN = KS == 2;                // the stage reads u^n
+  static_assert(!UN || kRingPD == 1, "the 2-slot u^n ring assumes one ring row in flight");
   constexpr int W = NT + 2;
   extern __shared__ double smem[];
   double* ring = smem;                               // [kRingRows][NC][W]
-  constexpr bool kFaceBuf = WENO && NT != 32;       // one-warp blocks exchange faces by shuffle
+  // x faces: one-warp blocks exchange them by shuffle; wider blocks shuffle
+  // inside each warp and pass only the high face of every warp's last lane
+  // through shared memory (kXShfl), or stage all faces (hx / lx)
+  constexpr bool kFaceBuf = WENO && NT != 32 && !kXShfl<NT>;
   double* hx = ring + kRingRows * NC * W;            // [NC][NT]
   double* lx = hx + (kFaceBuf ? NC * NT : 0);        // [NC][NT]
-  double* gx = lx + (kFaceBuf ? NC * NT : 0);        // [NC][NT]
-  double* nring = gx + NC * NT;                      // [3][NC][NT]: u^n rows for the RK combination
+  double* bnd = lx + (kFaceBuf ? NC * NT : 0);       // [NT/32][NC] (kXShfl)
+  double* gx = bnd + (WENO && kXShfl<NT> ? NC * (NT / 32) : 0);  // [NC][NT]
+  double* nring = gx + NC * NT;                      // [2][NC][NT]: u^n rows for the RK combination
   // march recurrence (high face H and flux G of the previous row) lives in
   // shared memory, not registers: it is idle during the whole x sweep
-  double* hs = nring + 3 * NC * NT;                  // [NC][NT]
+  double* hs = nring + 2 * NC * NT;                  // [NC][NT]
   double* gs = hs + NC * NT;                         // [NC][NT]
   auto RG = [&](int slot, int c, int x) -> double& { return ring[(slot * NC + c) * W + x]; };
   auto NR = [&](int slot, int c) -> double& { return nring[(slot * NC + c) * NT + threadIdx.x]; };
@@ -813,37 +843,40 @@ ring_kernel(const StageParams p) {
     sts[i] = p.st + (p.shared_state ? 0 : inst + i);
     act[i] = !*(volatile int*)&sts[i]->done;
     any = any || act[i];
-    dts[i] = p.kind == 0 ? 0.0 : *(volatile double*)&sts[i]->dt;
+    dts[i] = KS == 0 ? 0.0 : *(volatile double*)&sts[i]->dt;
   }
   if (!any) return;
   const double dt = dts[0];
-  const int64_t cs = NI > 1 ? p.si : p.sc;  // stride between the components held here
+  // 32-bit element offsets inside one instance (fvb_capi.cu checks the
+  // instance fits); one 64-bit base per block
+  const int cs = (int)(NI > 1 ? p.si : p.sc);  // stride between the components held here
   const double* __restrict__ us = p.us + p.origin + inst * p.si;
   const double* un = p.un + p.origin + inst * p.si;
   double* out = p.out + p.origin + inst * p.si;
   const int tx = threadIdx.x;
-  const int64_t x0 = (int64_t)blockIdx.x * (NT - 2);
-  const int64_t xf = x0 - 1 + tx;
-  const bool cell = tx >= 1 && tx <= NT - 2 && xf < p.n[0];
-  const int64_t ra = p.row_lo + (int64_t)blockIdx.y * p.H;
-  const int64_t rb = min(ra + (int64_t)p.H, p.row_hi);
-  const int64_t co = map_index(xf, p.n[0], p.bc[0], p.g);
+  const int x0 = blockIdx.x * (NT - 2);
+  const int xf = x0 - 1 + tx;
+  const int nx = (int)p.n[0];
+  const bool cell = tx >= 1 && tx <= NT - 2 && xf < nx;
+  const int ra = (int)p.row_lo + blockIdx.y * p.H;
+  const int rb = min(ra + p.H, (int)p.row_hi);
+  const int co = (int)map_index(xf, nx, p.bc[0], p.g);
   // halo columns: thread 0 also copies x0-2, thread NT-1 also x0+NT-1
   const bool halo_t = WENO && (tx == 0 || tx == NT - 1);
-  const int64_t hco = map_index(tx == 0 ? x0 - 2 : x0 + NT - 1, p.n[0], p.bc[0], p.g);
+  const int hco = (int)map_index(tx == 0 ? x0 - 2 : x0 + NT - 1, nx, p.bc[0], p.g);
   const int hcol = tx == 0 ? 0 : NT + 1;
   // row offsets of rows ra-2 .. rb+PD+1, computed once per block
-  int64_t* rtab = reinterpret_cast<int64_t*>(gs + NC * NT);
-  for (int i = tx; i < p.H + kRingPD + 4; i += NT) rtab[i] = map_index(ra - 2 + i, p.n[1], p.bc[1], p.g) * p.sy;
+  int* rtab = reinterpret_cast<int*>(gs + NC * NT);
+  for (int i = tx; i < p.H + kRingPD + 4; i += NT) rtab[i] = (int)(map_index(ra - 2 + i, p.n[1], p.bc[1], p.g) * p.sy);
   __syncthreads();
-  auto roff = [&](int64_t r) -> int64_t { return rtab[r - (ra - 2)]; };
-  auto fetch = [&](int64_t r, int slot) {  // async copy of row r into a ring slot
-    const int64_t ro = roff(r);
+  auto roff = [&](int r) -> int { return rtab[r - (ra - 2)]; };
+  auto fetch = [&](int r, int slot) {  // async copy of row r into a ring slot
+    const int ro = roff(r);
 #pragma unroll
-    for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, tx + 1), us + co + ro + c * cs);
+    for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, tx + 1), us + (co + ro + c * cs));
     if (halo_t) {
 #pragma unroll
-      for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, hcol), us + hco + ro + c * cs);
+      for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, hcol), us + (hco + ro + c * cs));
     }
   };
 
@@ -854,33 +887,43 @@ ring_kernel(const StageParams p) {
     errbs[i] = 0;
     smaxs[i][0] = smaxs[i][1] = 0.0;
   }
-  // RK stage as a*u^n + b*(u^s + dt L) (solver.py:166-173); fast mode only
+  // RK stage as a*u^n + b*(u^s + dt L) (solver.py:166-173); fast mode folds
+  // b, dt and 1/delta into the flux differences
   const double rk_a = p.kind == 2 ? 0.5 : (p.kind == 3 ? 0.75 : (p.kind == 4 ? 1.0 / 3.0 : 0.0));
   const double rk_b = p.kind == 2 ? 0.5 : (p.kind == 3 ? 0.25 : (p.kind == 4 ? 2.0 / 3.0 : 1.0));
+#if FVB_FAST
+  const double cx = KS == 0 ? p.id[0] : (KS == 1 ? dt * p.id[0] : rk_b * dt * p.id[0]);
+  const double cy = KS == 0 ? p.id[1] : (KS == 1 ? dt * p.id[1] : rk_b * dt * p.id[1]);
+#endif
 
   // prologue: rows ra-2 .. ra-1+PD (slot of row r = (r - ra + 2) % kRingRows)
   for (int k = 0; k < kRingPD + 2; ++k) {
     fetch(ra - 2 + k, k);
     cp_async_commit();
   }
-  int sA = 0;  // slot of row r-1 at the top of the loop (r = ra-1 -> row ra-2)
-  for (int64_t r = ra - 1; r <= rb; ++r) {
+  int sA = 0;   // slot of row r-1 at the top of the loop (r = ra-1 -> row ra-2)
+  int nsw = 1;  // u^n slot written this iteration (row r): (r - ra) & 1
+                // -- each thread's own column: no cross-thread hazard
+  for (int r = ra - 1; r <= rb; ++r) {
     const int sB = sA + 1 == kRingRows ? 0 : sA + 1;
     const int sC = sB + 1 == kRingRows ? 0 : sB + 1;
     // iteration ra-1 has no in-plane barrier: make sure its reads of the
     // slot about to be refilled (row ra-2) are done
     if (r == ra) __syncthreads();
     // issue row r+1+PD into the slot that held row r-2 (free since last row),
-    // and u^n of row r+1 (consumed two iterations later) into its 3-slot ring
+    // and u^n of row r (consumed by the next iteration's finish) into its
+    // 2-slot ring
     {
       int sN = sC + kRingPD;  // slot(row) = (row - ra + 2) % kRingRows -> the slot of row r-2
       sN = sN >= kRingRows ? sN - kRingRows : sN;
       if (r + 1 + kRingPD <= rb + 1) fetch(r + 1 + kRingPD, sN);
-      if (p.kind >= 2 && cell && r + 1 >= ra && r + 1 < rb) {
-        const int64_t o = co + roff(r + 1);
-        const int ns = (int)((r + 1 - ra) % 3);
+      if constexpr (UN) {
+        nsw ^= 1;
+        if (cell && r >= ra && r < rb) {
+          const int o = co + roff(r);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) cp_async8(&NR(ns, c), un + o + c * cs);
+          for (int c = 0; c < NC; ++c) cp_async8(&NR(nsw, c), un + (o + c * cs));
+        }
       }
       cp_async_commit();
     }
@@ -890,14 +933,6 @@ ring_kernel(const StageParams p) {
     // side effects are predicated on `cell`: no divergent regions, so no
     // reconvergence bookkeeping in the hot loop.
     const bool fin = cell && r - 1 >= ra;
-    double unc[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) unc[c] = 0.0;
-    if (p.kind >= 2 && r - 1 >= ra) {  // u^n of row r-1 landed with the group of iteration r-2
-      const int ns = (int)((r - 1 - ra) % 3);
-#pragma unroll
-      for (int c = 0; c < NC; ++c) unc[c] = NR(ns, c);
-    }
     {  // march (y) direction: faces of row r, flux (r-1|r), finish row r-1
       double A[NC], B[NC], C[NC], hi[NC], lo[NC];
 #pragma unroll
@@ -923,36 +958,51 @@ ring_kernel(const StageParams p) {
             if (eb && cell) errbs[i] |= 2u;
           }
         }
+        double unc[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) unc[c] = 0.0;
+        if constexpr (UN) {
+          if (r - 1 >= ra) {  // u^n of row r-1 landed with the group of iteration r-1
+#pragma unroll
+            for (int c = 0; c < NC; ++c) unc[c] = NR(nsw ^ 1, c);
+          }
+        }
         double v[NC];
         const int tr = tx + 1 < NT ? tx + 1 : NT - 1;
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          // x residual of row r-1 straight from its fluxes (still in gx)
           const double Gp = gs[c * NT + tx];
+#if FVB_FAST
+          // x: gx holds the raw fluxes (two-warp blocks) or this column's own
+          // difference (shuffle x sweep, already scaled by 1/dx)
+          if constexpr (NI == 1) {
+            double base = KS == 0 ? 0.0 : (KS == 1 ? A[c] : fma(rk_b, A[c], rk_a * unc[c]));
+            if constexpr (kShflX) {
+              base = fma(KS == 0 ? 1.0 : (KS == 1 ? dt : rk_b * dt), gx[c * NT + tx], base);
+            } else {
+              base = fma(cx, gx[c * NT + tx] - gx[c * NT + tr], base);
+            }
+            v[c] = fma(cy, Gp - GC[c], base);
+          } else {  // per-instance dt (the instances of a batch differ)
+            const double dtc = dts[c];
+            const double xs = kShflX ? gx[c * NT + tx] : (gx[c * NT + tx] - gx[c * NT + tr]) * p.id[0];
+            const double Lc = fma(Gp - GC[c], p.id[1], xs);
+            v[c] = KS == 0 ? Lc : (KS == 1 ? fma(dtc, Lc, A[c]) : fma(rk_a, unc[c], rk_b * fma(dtc, Lc, A[c])));
+          }
+#else
           double xres;
           if constexpr (kShflX) {
             xres = gx[c * NT + tx];  // this column's own, computed by the x sweep
           } else {
             const double g0 = gx[c * NT + tx], g1 = gx[c * NT + tr];
-#if FVB_FAST
-            xres = (g0 - g1) * p.id[0];
-#else
             xres = 0.0 - ddiv(g1 - g0, p, 0);
-#endif
           }
-#if FVB_FAST
-          const double Lc = fma(Gp - GC[c], p.id[1], xres);
-#else
           const double Lc = xres - ddiv(GC[c] - Gp, p, 1);
-#endif
-#if FVB_FAST
-          v[c] = p.kind == 0 ? Lc : fma(rk_a, unc[c], rk_b * fma(NI > 1 ? dts[c] : dt, Lc, A[c]));
-#else
-          v[c] = rk_combine(p.kind, unc[c], A[c], NI > 1 ? dts[c] : dt, Lc);
+          v[c] = KS == 0 ? Lc : rk_combine(p.kind, unc[c], A[c], NI > 1 ? dts[c] : dt, Lc);
 #endif
         }
         if (fin) {
-          const int64_t o = co + roff(r - 1);
+          const int o = co + roff(r - 1);
           if constexpr (NI == 1) {
 #pragma unroll
             for (int c = 0; c < NC; ++c) out[o + c * cs] = v[c];
@@ -1013,13 +1063,13 @@ ring_kernel(const StageParams p) {
           };
           unsigned eb = 0;
           interface_flux_lazy<EQ, FLUX, DIM, RECON>(uL, uR, cells, 0, p.P, Gx, eb);
-          if (eb && tx >= 1 && xf <= p.n[0]) errb |= 1u;
+          if (eb && tx >= 1 && xf <= nx) errb |= 1u;
         } else {
 #pragma unroll
           for (int i = 0; i < NI; ++i) {
             unsigned eb = 0;
             interface_flux<EQ, FLUX, DIM, RECON>(uL + i, uR + i, uL + i, uR + i, 0, p.P, Gx + i, eb);
-            if (eb && tx >= 1 && xf <= p.n[0]) errbs[i] |= 1u;
+            if (eb && tx >= 1 && xf <= nx) errbs[i] |= 1u;
           }
         }
 #pragma unroll
@@ -1032,6 +1082,7 @@ ring_kernel(const StageParams p) {
 #endif
         }
       } else {
+      double uL[NC], uR[NC];
       if constexpr (WENO) {
         double um[NC], uc[NC], up[NC], hi[NC], lo[NC];
 #pragma unroll
@@ -1041,21 +1092,38 @@ ring_kernel(const StageParams p) {
           up[c] = RG(sB, c, tx + 2);
         }
         weno_faces_nc<NC, RECON>(um, uc, up, p.P.eps, hi, lo);
+        if constexpr (kXShfl<NT>) {
+          const int lane = tx & 31;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          hx[c * NT + tx] = hi[c];
-          lx[c * NT + tx] = lo[c];
+          for (int c = 0; c < NC; ++c) {
+            uR[c] = lo[c];
+            uL[c] = __shfl_up_sync(0xffffffffu, hi[c], 1);
+            if (lane == 31) bnd[(tx >> 5) * NC + c] = hi[c];
+          }
+          __syncthreads();
+          if (lane == 0 && tx > 0) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) uL[c] = bnd[((tx >> 5) - 1) * NC + c];
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            hx[c * NT + tx] = hi[c];
+            lx[c * NT + tx] = lo[c];
+          }
+          __syncthreads();
         }
-        __syncthreads();
       }
       if constexpr (!WENO) __syncthreads();  // every lane has read row r-1's gx
       {  // x interface tx sits between face cells tx-1 and tx (lane 0's is unused)
         const int tl = tx >= 1 ? tx - 1 : 0;
-        double uL[NC], uR[NC], Gx[NC];
+        double Gx[NC];
+        if constexpr (!(WENO && kXShfl<NT>)) {
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          uL[c] = WENO ? hx[c * NT + tl] : RG(sB, c, tx);
-          uR[c] = WENO ? lx[c * NT + tx] : RG(sB, c, tx + 1);
+          for (int c = 0; c < NC; ++c) {
+            uL[c] = WENO ? hx[c * NT + tl] : RG(sB, c, tx);
+            uR[c] = WENO ? lx[c * NT + tx] : RG(sB, c, tx + 1);
+          }
         }
         if constexpr (NI == 1) {
           auto cells = [&](double* a, double* b) {  // fallback only: loaded on demand
@@ -1067,13 +1135,13 @@ ring_kernel(const StageParams p) {
           };
           unsigned eb = 0;
           interface_flux_lazy<EQ, FLUX, DIM, RECON>(uL, uR, cells, 0, p.P, Gx, eb);
-          if (eb && tx >= 1 && xf <= p.n[0]) errb |= 1u;
+          if (eb && tx >= 1 && xf <= nx) errb |= 1u;
         } else {  // scalar laws: no positivity fallback, the cells are never read
 #pragma unroll
           for (int i = 0; i < NI; ++i) {
             unsigned eb = 0;
             interface_flux<EQ, FLUX, DIM, RECON>(uL + i, uR + i, uL + i, uR + i, 0, p.P, Gx + i, eb);
-            if (eb && tx >= 1 && xf <= p.n[0]) errbs[i] |= 1u;
+            if (eb && tx >= 1 && xf <= nx) errbs[i] |= 1u;
           }
         }
 #pragma unroll
@@ -1115,8 +1183,9 @@ ring_kernel(const StageParams p) {
 template <int EQ, int RECON, int NT, int NI = 1>
 constexpr int ring_smem_bytes() {
   constexpr int NC = NComp<EQ, 2>::value * NI;
-  return 8 * (kRingRows * NC * (NT + 2) + (RECON != RECON_NONE && NT != 32 ? 2 : 0) * NC * NT + NC * NT +
-              3 * NC * NT + 2 * NC * NT);
+  constexpr bool weno = RECON != RECON_NONE;
+  return 8 * (kRingRows * NC * (NT + 2) + (weno && NT != 32 && !kXShfl<NT> ? 2 : 0) * NC * NT +
+              (weno && kXShfl<NT> ? NC * (NT / 32) : 0) + NC * NT + 2 * NC * NT + 2 * NC * NT);
 }
 
 // ---------------------------------------------------------------------------

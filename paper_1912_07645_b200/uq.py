@@ -618,6 +618,8 @@ def run_mlmc(plan, make_cfg, evaluate_init, workers: int = 1, *, batch: int | No
 def _merge_ranks(slots, dist, group, world):
     """Deterministic cross-rank reduce: one all_gather per statistic, then a
     fold in rank order (rank 0's sample block first)."""
+    import torch
+
     for s in slots:
         g = s.gpu
         if isinstance(g, FieldMoments):
@@ -636,5 +638,22 @@ def _merge_ranks(slots, dist, group, world):
                 tot._sums += sums
                 tot.samples += cnt
             s.gpu = tot
+        elif s.kind == "histogram":
+            # counts and sample totals add (uq.py:221-228): all-gather, sum in rank order
+            h = s.hist
+            counts = torch.as_tensor(np.ascontiguousarray(h.counts), dtype=torch.int64)
+            counts = counts.to("cuda") if dist.get_backend(group) == "nccl" else counts
+            blocks = gather_ordered([counts], h.samples, dist, group, world)
+            tot = np.zeros_like(h.counts)
+            for cnt, (c,) in blocks:
+                tot = tot + c.cpu().numpy().astype(h.counts.dtype)
+            h.counts = tot
+            h.samples = sum(cnt for cnt, _ in blocks)
         else:
-            raise E.ConfigError(f"functional {s.kind!r} cannot be merged across ranks")
+            # any other host functional: gather the objects, merge in rank order
+            objs = [None] * world
+            dist.all_gather_object(objs, s.host, group=group)
+            tot = s.proto.fresh()
+            for o in objs:
+                tot.merge(o)
+            s.host = tot

@@ -136,3 +136,62 @@ def test_halo_exchange_dist_gloo(lay, periodic):
     out = mgr.dict()
     mp.spawn(_halo_worker, args=(world, _free_port(), lay, periodic, out), nprocs=world, join=True)
     assert all(out[r] for r in range(world))
+
+
+class _CountFunctional:
+    """A host-side functional of the duck-typed reference protocol
+    (fresh/update/merge/name, uq.py:161-273) that run_mc feeds host fields."""
+
+    name = "count_max"
+
+    def __init__(self):
+        self.samples = 0
+        self.maxima = []
+
+    def fresh(self):
+        return _CountFunctional()
+
+    def update(self, field):
+        self.samples += 1
+        self.maxima.append(float(np.max(field.data)))
+
+    def merge(self, other):
+        self.samples += other.samples
+        self.maxima += other.maxima
+
+
+def _merge_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1912_07645_b200 import uq
+
+    proto_h = uq.Histogram([(1, 2), (3, 0)], 0, 0.0, 1.0, bins=4)
+    proto_c = _CountFunctional()
+    slots = [uq._Slot(proto_h, None, 1), uq._Slot(proto_c, None, 1)]
+    rng = np.random.default_rng(11)
+    vals = rng.uniform(-0.2, 1.2, size=(9, 2))  # 9 samples, 2 probes each
+    lo, hi = shard_range(len(vals), world, rank)
+    for k in range(lo, hi):
+        slots[0].hist.add_values(vals[k])
+        slots[1].host.samples += 1
+        slots[1].host.maxima.append(float(vals[k].max()))
+    uq._merge_ranks(slots, dist, None, world)
+    ref = uq.Histogram([(1, 2), (3, 0)], 0, 0.0, 1.0, bins=4)
+    for v in vals:
+        ref.add_values(v)
+    h, c = slots[0].result(), slots[1].result()
+    out[rank] = (bool(np.array_equal(h.counts, ref.counts)) and h.samples == 9 and c.samples == 9
+                 and c.maxima == [float(v.max()) for v in vals])
+    dist.destroy_process_group()
+
+
+def test_histogram_and_host_functional_merge_gloo():
+    """run_mc's cross-rank merge of a Histogram (counts and samples add) and
+    of an arbitrary host functional (gathered, merged in rank order =
+    sample order), ADVICE r01."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_merge_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert out[0] and out[1]

@@ -28,30 +28,37 @@ __global__ void k(double* out, int n) {
   double s2 = x * y2;
   double s2c = fma(fma(-s2, s2, x), 0.5 * y2, s2);
   double sq = sqrt(x);
-  out[i * 7 + 0] = fabs(r - ex) / ex;
-  out[i * 7 + 1] = fabs(r1 - ex) / ex;
-  out[i * 7 + 2] = fabs(r3 - ex) / ex;
+  // fvb_physics.cuh fsqrt (fast mode): one third-order step on s = x*y
+  double s3 = x * y;
+  double e3 = fma(-s3, y, 1.0);
+  s3 = fma(s3 * e3, fma(e3, 0.375, 0.5), s3);
+  out[i * 9 + 7] = fabs(s3 - sq) / sq;
+  out[i * 9 + 8] = fabs(s3 - sq) / (nextafter(sq, 1e300) - sq);  // ulps
+  out[i * 9 + 0] = fabs(r - ex) / ex;
+  out[i * 9 + 1] = fabs(r1 - ex) / ex;
+  out[i * 9 + 2] = fabs(r3 - ex) / ex;
   (void)r2;
-  out[i * 7 + 3] = fabs(y - ey) / ey;
-  out[i * 7 + 4] = fabs(s1c - sq) / sq;
-  out[i * 7 + 5] = fabs(s2c - sq) / sq;
-  out[i * 7 + 6] = (s1c == sq) ? 0.0 : 1.0;
+  out[i * 9 + 3] = fabs(y - ey) / ey;
+  out[i * 9 + 4] = fabs(s1c - sq) / sq;
+  out[i * 9 + 5] = fabs(s2c - sq) / sq;
+  out[i * 9 + 6] = (s1c == sq) ? 0.0 : 1.0;
 }
 int main() {
   const int n = 1 << 22;
   double* d;
-  cudaMalloc(&d, sizeof(double) * 7 * n);
+  cudaMalloc(&d, sizeof(double) * 9 * n);
   k<<<n / 256, 256>>>(d, n);
-  double* h = new double[7 * (size_t)n];
-  cudaMemcpy(h, d, sizeof(double) * 7 * n, cudaMemcpyDeviceToHost);
-  double mx[7] = {0};
+  double* h = new double[9 * (size_t)n];
+  cudaMemcpy(h, d, sizeof(double) * 9 * n, cudaMemcpyDeviceToHost);
+  double mx[9] = {0};
   double cnt = 0;
   for (int i = 0; i < n; ++i) {
-    for (int j = 0; j < 6; ++j) mx[j] = fmax(mx[j], h[i * 7 + j]);
-    cnt += h[i * 7 + 6];
+    for (int j = 0; j < 9; ++j) if (j != 6) mx[j] = fmax(mx[j], h[i * 9 + j]);
+    cnt += h[i * 9 + 6];
   }
   printf("rcp seed %.3e  1NR %.3e  cubic %.3e\n", mx[0], mx[1], mx[2]);
   printf("rsq seed %.3e  sqrt(1NR+corr) %.3e  sqrt(2NR+corr) %.3e  (1NR+corr != sqrt in %.4f%%)\n", mx[3], mx[4],
          mx[5], 100.0 * cnt / n);
+  printf("sqrt(third-order step) max rel %.3e  max ulp %.2f\n", mx[7], mx[8]);
   return 0;
 }
