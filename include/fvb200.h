@@ -226,6 +226,21 @@ int fvb_halo_unpack(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, do
                     int axis, int side, const double* buf);
 int64_t fvb_halo_count(const fvb_scheme* s, int axis);
 
+/* numerics.py:133-196 rusanov_flux / hllc_flux (FLUX_FUNCTIONS, the
+ * reference's flux registry seam, numerics.py:199-206) on n face pairs:
+ * uL, uR, F are (ncomp, n) component-major device arrays.  Uses s->dim,
+ * ncomp, eq, flux, gamma, adv, arith.  FVB_E_UNPHYSICAL for a degenerate
+ * HLLC wave fan (numerics.py:166-167), FVB_E_CONFIG for HLLC on a scalar law
+ * (numerics.py:150-151). */
+int fvb_face_flux(fvb_ctx* ctx, const fvb_scheme* s, int axis, const double* uL, const double* uR, int64_t n,
+                  double* F);
+/* numerics.py:64-87 weno_weights + weno_face_value, elementwise over n
+ * stencils (um, uc, up): w0, w1 (nullable) and the downwind face value
+ * (nullable).  s->recon selects WENO2/WENO3 ideal weights, s->weno_eps the
+ * epsilon; exact arithmetic follows the reference op by op. */
+int fvb_weno(fvb_ctx* ctx, const fvb_scheme* s, const double* um, const double* uc, const double* up, int64_t n,
+             double* w0, double* w1, double* face);
+
 #ifdef __cplusplus
 }
 #endif

@@ -99,6 +99,10 @@ _SIGS = {
     "fvb_halo_unpack": ([C.c_void_p, C.POINTER(Scheme), C.POINTER(Layout), C.c_void_p, C.c_int, C.c_int,
                          C.c_void_p], C.c_int),
     "fvb_halo_count": ([C.POINTER(Scheme), C.c_int], C.c_int64),
+    "fvb_face_flux": ([C.c_void_p, C.POINTER(Scheme), C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
+                      C.c_int),
+    "fvb_weno": ([C.c_void_p, C.POINTER(Scheme), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                  C.c_void_p, C.c_void_p], C.c_int),
 }
 
 EXPORTS = tuple(_SIGS)

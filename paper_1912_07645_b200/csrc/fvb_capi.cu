@@ -18,11 +18,19 @@
 
 namespace fvb {
 namespace exact {
+int launch_face_flux(int dim, int eq, int flux, const Phys& P, int axis, const double* uL, const double* uR,
+                     int64_t n, double* F, unsigned long long* err, cudaStream_t s);
+int launch_weno(int recon, double eps, const double* um, const double* uc, const double* up, int64_t n, double* w0,
+                double* w1, double* face, cudaStream_t s);
 int launch_stage(int dim, int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s);
 int launch_speed(int dim, int eq, const StageParams& p, int finalize, dim3 grid, cudaStream_t s);
 void stage_block(int dim, int eq, int variant, int& nt, int& nty);
 }  // namespace exact
 namespace fast {
+int launch_face_flux(int dim, int eq, int flux, const Phys& P, int axis, const double* uL, const double* uR,
+                     int64_t n, double* F, unsigned long long* err, cudaStream_t s);
+int launch_weno(int recon, double eps, const double* um, const double* uc, const double* up, int64_t n, double* w0,
+                double* w1, double* face, cudaStream_t s);
 int launch_stage(int dim, int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s);
 int launch_speed(int dim, int eq, const StageParams& p, int finalize, dim3 grid, cudaStream_t s);
 void stage_block(int dim, int eq, int variant, int& nt, int& nty);
@@ -616,7 +624,6 @@ int fvb_run_begin(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, doub
   r = validate_instances(ctx, s, lay, ninst, false);
   if (r) return r;
   destroy_graph(ctx);
-  ctx->launches = 0;
   r = ensure_state(ctx, ninst);
   if (r) return r;
   r = reset_states(ctx, ctx->d_state, ninst, 0.0);
@@ -971,3 +978,54 @@ int fvb_halo_unpack(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, do
 int64_t fvb_halo_count(const fvb_scheme* s, int axis) { return fvb::halo_count(*s, axis); }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// numerics.py function-level entry points (the FLUX_FUNCTIONS seam)
+// ---------------------------------------------------------------------------
+
+int fvb_face_flux(fvb_ctx* ctx, const fvb_scheme* s, int axis, const double* uL, const double* uR, int64_t n,
+                  double* F) {
+  if (!s) return set_err(ctx, FVB_E_CONFIG, "null scheme");
+  if (s->dim < 1 || s->dim > 3) return set_err(ctx, FVB_E_CONFIG, "dim must be 1, 2 or 3, got %d", s->dim);
+  if (axis < 0 || axis >= s->dim) return set_err(ctx, FVB_E_CONFIG, "axis %d out of range", axis);
+  if (s->flux == FVB_FLUX_HLLC && s->eq != FVB_EQ_EULER)
+    return set_err(ctx, FVB_E_CONFIG, "HLLC flux is only defined for the Euler equations");
+  fvb::Phys P;
+  P.gamma = s->gamma;
+  P.gm1 = s->gamma - 1.0;
+  P.eps = s->weno_eps;
+  for (int k = 0; k < 3; ++k) P.adv[k] = s->adv[k];
+  // three scratch words (no single-shot call is in flight): degenerate flag,
+  // first unphysical uL / uR face
+  unsigned long long* d_err = reinterpret_cast<unsigned long long*>(ctx->d_scratch_state);
+  const unsigned long long init[3] = {0ull, ~0ull, ~0ull};
+  CUDA_TRY(ctx, cudaMemcpyAsync(d_err, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+  const int r = s->arith == FVB_ARITH_FAST
+                    ? fvb::fast::launch_face_flux(s->dim, s->eq, s->flux, P, axis, uL, uR, n, F, d_err, ctx->stream)
+                    : fvb::exact::launch_face_flux(s->dim, s->eq, s->flux, P, axis, uL, uR, n, F, d_err, ctx->stream);
+  if (r) return set_err(ctx, FVB_E_CONFIG, "unsupported equation/flux combination");
+  ctx->launches++;
+  int rc = check_launch(ctx, "face_flux");
+  if (rc) return rc;
+  unsigned long long h[3];
+  CUDA_TRY(ctx, cudaMemcpyAsync(h, d_err, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  // the reference evaluates physical_flux(uL), physical_flux(uR), then the fan check
+  if (h[1] != ~0ull) return set_err(ctx, FVB_E_UNPHYSICAL, "unphysical state: side L face %llu", h[1]);
+  if (h[2] != ~0ull) return set_err(ctx, FVB_E_UNPHYSICAL, "unphysical state: side R face %llu", h[2]);
+  if (h[0]) return set_err(ctx, FVB_E_UNPHYSICAL, "degenerate HLLC wave fan (sL >= sR)");
+  return FVB_OK;
+}
+
+int fvb_weno(fvb_ctx* ctx, const fvb_scheme* s, const double* um, const double* uc, const double* up, int64_t n,
+             double* w0, double* w1, double* face) {
+  if (!s) return set_err(ctx, FVB_E_CONFIG, "null scheme");
+  if (s->recon != FVB_RECON_WENO2 && s->recon != FVB_RECON_WENO3)
+    return set_err(ctx, FVB_E_CONFIG, "weno_weights needs WENO2 or WENO3");
+  const int r = s->arith == FVB_ARITH_FAST
+                    ? fvb::fast::launch_weno(s->recon, s->weno_eps, um, uc, up, n, w0, w1, face, ctx->stream)
+                    : fvb::exact::launch_weno(s->recon, s->weno_eps, um, uc, up, n, w0, w1, face, ctx->stream);
+  if (r) return set_err(ctx, FVB_E_CONFIG, "unsupported reconstruction");
+  ctx->launches++;
+  return check_launch(ctx, "weno");
+}

@@ -1,6 +1,8 @@
 // Instantiates the stage / wave-speed kernels for one arithmetic mode.
 // Built twice: -DFVB_FAST=0 -DFVB_NS=exact -fmad=false  (bitwise == reference)
 //              -DFVB_FAST=1 -DFVB_NS=fast  -fmad=true
+#include <algorithm>
+
 #include "fvb_stage.cuh"
 
 namespace fvb {
@@ -46,7 +48,9 @@ void stage_block(int dim, int eq, int variant, int& nt, int& nty) {
 // that would be launched (fvb_capi.cu stage_grid sizes the grid with it)
 template <typename K>
 static int occupancy(K kern, dim3 block, int smem) {
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  // raise (never lower) the opt-in limit: a later launch may need more
+  // (the per-block offset table grows with the march length)
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, (int)(block.x * block.y), smem) != cudaSuccess) n = 0;
   return n;
@@ -56,7 +60,7 @@ template <typename K>
 static int launch_pdl(K kern, dim3 grid, dim3 block, int smem, cudaStream_t s, const StageParams& p) {
   if (grid.x == 0) return occupancy(kern, block, smem);
   // wider ring blocks (-DFVB_RING_NT=96/128) need more than 48 KB
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 #if FVB_PDL
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
@@ -205,6 +209,82 @@ int launch_stage(int dim, int eq, int flux, int recon, const StageParams& p, dim
 #endif
 
 #if FVB_KDIM == 0
+// numerics.py:133-196 on arrays of face pairs (the FLUX_FUNCTIONS seam):
+// the stage kernels' own device flux functions, one face per thread.
+// err[0]: degenerate HLLC fan seen; err[1] / err[2]: lowest face index with
+// an unphysical uL / uR state (physical_flux's check, equations.py:91-99).
+template <int EQ, int FLUX, int DIM>
+__global__ void face_flux_kernel(Phys P, int axis, const double* __restrict__ uL, const double* __restrict__ uR,
+                                 int64_t n, double* __restrict__ F, unsigned long long* err) {
+  constexpr int NC = NComp<EQ, DIM>::value;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double a[NC], b[NC], f[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      a[c] = uL[c * n + i];
+      b[c] = uR[c * n + i];
+    }
+    unsigned eb = 0;
+    if constexpr (EQ == EQ_EULER) {
+      if (!((a[0] > kFloor) & (euler_pressure<DIM>(a, P) > kFloor))) atomicMin(err + 1, (unsigned long long)i);
+      if (!((b[0] > kFloor) & (euler_pressure<DIM>(b, P) > kFloor))) atomicMin(err + 2, (unsigned long long)i);
+      const EState L = euler_state<DIM>(a, axis, P);
+      const EState R = euler_state<DIM>(b, axis, P);
+      if constexpr (FLUX == FLUX_HLLC) hllc<DIM>(a, b, L, R, axis, P, f, eb, bits_equal_all<NC>(a, b));
+      else rusanov<EQ, DIM>(a, b, L, R, axis, P, f);
+    } else {
+      EState d{};
+      rusanov<EQ, DIM>(a, b, d, d, axis, P, f);
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) F[c * n + i] = f[c];
+    if (eb) atomicOr(err, 1ull);
+  }
+}
+
+template <int RECON>
+__global__ void weno_kernel(double eps, const double* __restrict__ um, const double* __restrict__ uc,
+                            const double* __restrict__ up, int64_t n, double* w0, double* w1, double* face) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double m = um[i], c = uc[i], q = up[i];
+    // numerics.py:64-87, operation by operation
+    constexpr double d0 = RECON == RECON_WENO2 ? 0.5 : 1.0 / 3.0, d1 = RECON == RECON_WENO2 ? 0.5 : 2.0 / 3.0;
+    const double D0 = c - m, D1 = q - c;
+    const double e0 = eps + D0 * D0, e1 = eps + D1 * D1;
+    const double a0 = d0 / (e0 * e0), a1 = d1 / (e1 * e1);
+    const double tot = a0 + a1;
+    const double x0 = a0 / tot, x1 = a1 / tot;
+    if (w0) w0[i] = x0;
+    if (w1) w1[i] = x1;
+    if (face) face[i] = c + 0.5 * (x0 * D0 + x1 * D1);
+  }
+}
+
+int launch_face_flux(int dim, int eq, int flux, const Phys& P, int axis, const double* uL, const double* uR,
+                     int64_t n, double* F, unsigned long long* err, cudaStream_t s) {
+  const int blocks = (int)std::min<int64_t>((n + 127) / 128, 148 * 16);
+  if (n <= 0) return 0;
+#define FVB_FF(E, FL, D) \
+  if (eq == E && flux == FL && dim == D) { face_flux_kernel<E, FL, D><<<blocks, 128, 0, s>>>(P, axis, uL, uR, n, F, err); return 0; }
+  FVB_FF(EQ_EULER, FLUX_HLLC, 1) FVB_FF(EQ_EULER, FLUX_HLLC, 2) FVB_FF(EQ_EULER, FLUX_HLLC, 3)
+  FVB_FF(EQ_EULER, FLUX_RUSANOV, 1) FVB_FF(EQ_EULER, FLUX_RUSANOV, 2) FVB_FF(EQ_EULER, FLUX_RUSANOV, 3)
+  FVB_FF(EQ_BURGERS, FLUX_RUSANOV, 1) FVB_FF(EQ_BURGERS, FLUX_RUSANOV, 2) FVB_FF(EQ_BURGERS, FLUX_RUSANOV, 3)
+  FVB_FF(EQ_ADVECTION, FLUX_RUSANOV, 1) FVB_FF(EQ_ADVECTION, FLUX_RUSANOV, 2)
+  FVB_FF(EQ_ADVECTION, FLUX_RUSANOV, 3)
+#undef FVB_FF
+  return -1;
+}
+
+int launch_weno(int recon, double eps, const double* um, const double* uc, const double* up, int64_t n, double* w0,
+                double* w1, double* face, cudaStream_t s) {
+  if (n <= 0) return 0;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (recon == RECON_WENO2) weno_kernel<RECON_WENO2><<<blocks, 256, 0, s>>>(eps, um, uc, up, n, w0, w1, face);
+  else if (recon == RECON_WENO3) weno_kernel<RECON_WENO3><<<blocks, 256, 0, s>>>(eps, um, uc, up, n, w0, w1, face);
+  else return -1;
+  return 0;
+}
+
 template <int DIM>
 static int launch_speed_dim(int eq, const StageParams& p, int fin, dim3 grid, cudaStream_t s) {
   if (eq == EQ_EULER) speed_kernel<DIM, EQ_EULER><<<grid, 256, 0, s>>>(p, fin);

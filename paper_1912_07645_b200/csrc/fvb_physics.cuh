@@ -22,9 +22,12 @@
 #error "FVB_FAST must be defined to 0 or 1"
 #endif
 // Warp-uniform shortcuts (flat WENO stencils, uniform interface states, no
-// star state in the warp): 1 = take them when the whole warp agrees.
+// star state in the warp): 1 = take them when the whole warp agrees.  Off by
+// default: in a developed flow (the KH roll-up bench.py times) whole warps
+// rarely agree and the votes cost more than they save (KH2D 1024^2 at
+// t ~ 1: 22.7 Gcell-stage/s without vs 21.2 with, profiles/r02_variants.json).
 #ifndef FVB_WARP_SKIP
-#define FVB_WARP_SKIP 1
+#define FVB_WARP_SKIP 0
 #endif
 
 namespace fvb {

@@ -94,14 +94,14 @@ template <int EQ, int DIM, int NC>
 __device__ __forceinline__ void post_cell(const StageParams& p, FvbState* st, const double* v,
                                           int64_t x, int64_t y, int64_t z, double* smax) {
   const long long cell = flat_cell<DIM>(p, x, y, z);
-  const long long ncell = (long long)p.n[0] * p.n[1] * p.n[2];
-  bool finite = true;
+  // non-finite <=> exponent field all ones: one integer test per component,
+  // one (rare) branch for the first bad component
+  unsigned bad = 0u;
 #pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    if (!isfinite(v[c])) {
-      if (finite) atomicMin(&st->bad_nonfinite, (long long)c * ncell + cell);
-      finite = false;
-    }
+  for (int c = 0; c < NC; ++c) bad |= ((((unsigned)__double2hiint(v[c]) >> 20) & 0x7ffu) == 0x7ffu) ? (1u << c) : 0u;
+  if (bad) {
+    const long long ncell = (long long)p.n[0] * p.n[1] * p.n[2];
+    atomicMin(&st->bad_nonfinite, (long long)(__ffs(bad) - 1) * ncell + cell);
   }
   double s[DIM];
 #if FVB_FAST
@@ -933,12 +933,14 @@ ring_kernel(const StageParams p) {
     // side effects are predicated on `cell`: no divergent regions, so no
     // reconvergence bookkeeping in the hot loop.
     const bool fin = cell && r - 1 >= ra;
+    double B[NC];  // row r of this column: the march stencil's centre and the x sweep's
+#pragma unroll
+    for (int c = 0; c < NC; ++c) B[c] = RG(sB, c, tx + 1);
     {  // march (y) direction: faces of row r, flux (r-1|r), finish row r-1
-      double A[NC], B[NC], C[NC], hi[NC], lo[NC];
+      double A[NC], C[NC], hi[NC], lo[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         A[c] = RG(sA, c, tx + 1);
-        B[c] = RG(sB, c, tx + 1);
         C[c] = RG(sC, c, tx + 1);
       }
       weno_faces_nc<NC, RECON>(A, B, C, p.P.eps, hi, lo);
@@ -1026,9 +1028,6 @@ ring_kernel(const StageParams p) {
     if (r >= ra && r < rb) {  // in-plane (x) direction of row r, straight from the ring
       if constexpr (EQ == EQ_EULER) {
         if (p.check_input && cell) {
-          double B[NC];
-#pragma unroll
-          for (int c = 0; c < NC; ++c) B[c] = RG(sB, c, tx + 1);
           if (!euler_physical<DIM>(B, p.P))
             atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | flat_cell<DIM>(p, xf, r, 0));
         }
@@ -1040,7 +1039,7 @@ ring_kernel(const StageParams p) {
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
             um[c] = RG(sB, c, tx);
-            uc[c] = RG(sB, c, tx + 1);
+            uc[c] = B[c];
             up[c] = RG(sB, c, tx + 2);
           }
           weno_faces_nc<NC, RECON>(um, uc, up, p.P.eps, hi, uR);
@@ -1088,7 +1087,7 @@ ring_kernel(const StageParams p) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           um[c] = RG(sB, c, tx);
-          uc[c] = RG(sB, c, tx + 1);
+          uc[c] = B[c];
           up[c] = RG(sB, c, tx + 2);
         }
         weno_faces_nc<NC, RECON>(um, uc, up, p.P.eps, hi, lo);

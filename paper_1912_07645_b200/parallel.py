@@ -324,32 +324,41 @@ def start_halo_exchange(topo: RankTopology, rank: int, periodic, pack, alloc, di
     torch.distributed P2P (NCCL on GPUs; gloo in the CPU tests) and return
     a handle for ``finish_halo_exchange``.
 
-    ``pack(axis, side)`` returns the contiguous slab of the g interior layers
-    next to face (axis, side); ``alloc(axis)`` an empty receive buffer.  Axes
-    are exchanged concurrently (the residual never reads corner ghosts,
-    solver.py:99-104).  Ordering rule so that a pair of ranks that are
-    mutual neighbours on both sides (2 ranks on a periodic axis,
+    ``pack(axis, side)`` returns the slab(s) of the g interior layers next to
+    face (axis, side) -- one contiguous tensor or a list of them;
+    ``alloc(axis, side)`` the matching receive buffer(s) for the ghosts of
+    that side.  Axes are exchanged concurrently (the residual never reads
+    corner ghosts, solver.py:99-104).  Ordering rule so that a pair of ranks
+    that are mutual neighbours on both sides (2 ranks on a periodic axis,
     parallel.py:227-230) match: sends are issued by side (low, high),
     receives by the SENDER's side, i.e. high ghosts first.  World-edge sides
     without a neighbour are left to the caller (outflow)."""
     ops, recvs = [], []
+
+    def _list(x):
+        return x if isinstance(x, (list, tuple)) else [x]
+
     for axis in (range(topo.dim) if axes is None else axes):
         if topo.ranks_per_axis[axis] == 1:
             continue
         nb = [topo.neighbor(rank, axis, side, bool(periodic[axis])) for side in (0, 1)]
         for side in (0, 1):
             if nb[side] is not None:
-                ops.append(dist.P2POp(dist.isend, pack(axis, side), nb[side], group))
+                for t in _list(pack(axis, side)):
+                    ops.append(dist.P2POp(dist.isend, t, nb[side], group))
         for side in (1, 0):
             if nb[side] is not None:
-                buf = alloc(axis)
-                ops.append(dist.P2POp(dist.irecv, buf, nb[side], group))
+                buf = alloc(axis, side)
+                for t in _list(buf):
+                    ops.append(dist.P2POp(dist.irecv, t, nb[side], group))
                 recvs.append((axis, side, buf))
     reqs = dist.batch_isend_irecv(ops) if ops else []
     return reqs, recvs
 
 
 def finish_halo_exchange(handle, unpack):
+    """Complete the exchange: NCCL works make the current stream wait (no
+    host block); then ``unpack(axis, side, buf)`` places each slab."""
     reqs, recvs = handle
     for req in reqs:
         req.wait()
@@ -362,128 +371,269 @@ def halo_exchange_dist(topo: RankTopology, rank: int, periodic, pack, unpack, al
     finish_halo_exchange(start_halo_exchange(topo, rank, periodic, pack, alloc, dist, group, axes), unpack)
 
 
-def run_parallel_nccl(init, cfg, topo, parts, n_steps, *, arith=None, group=None, cpu_comm: bool = False,
-                      overlap: bool = True):
-    """One subdomain per process (rank r of the torch.distributed group owns
-    part r), stage-wise: halo exchange of every stage input, fused stage
-    kernel, then one all-reduce(MAX) of [maxima, error flags] per step and a
-    device finalisation that all ranks evaluate identically
-    (parallel.py:479-521).  ``cpu_comm`` stages the exchanged slabs and the
-    reduce through host memory (gloo), e.g. to test several ranks on one GPU
-    without GPU-side waits."""
-    import torch
-    import torch.distributed as dist
+class _Halos:
+    """Persistent halo buffers of one rank's subdomain.
 
-    rank = dist.get_rank(group)
-    part = parts[rank]
-    grid = part.grid
-    ncomp = init.ncomp
-    stream = torch.cuda.Stream()
-    torch.cuda.set_stream(stream)  # NCCL calls order after the library's kernels on this stream
-    local = scatter_field(init, [part])[0]
-    dev = DeviceField.from_host(local)
-    b0 = dev.data.unsqueeze(0).contiguous()
-    bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
-    ctx = N.context()
-    split = tuple(k for k in range(grid.dim) if topo.ranks_per_axis[k] > 1)
-    periodic = [int(_v(cfg.bc[k]) == "periodic") for k in range(grid.dim)]
-    ctx.check(ctx.lib.fvb_run_set_external_reduce(ctx.h, 1))
-    mode = N.MODE_FIXED if n_steps is not None else N.MODE_PAR_T_END
-    run = DeviceRun(grid, cfg, bufs, 1, mode, n_steps, arith, halo_axes=split, ctx=ctx)
-    s = run.scheme
-    L = run.layout
-    red = torch.zeros(grid.dim + 2, dtype=torch.float64, device="cuda")
+    The march axis (z in 3D, y in 2D) -- the split bench.py uses -- needs no
+    packing: for every component the g send layers and the g ghost layers
+    are contiguous slices of the field buffer, so NCCL reads and writes them
+    in place (ncomp messages per side).  Other axes go through fvb_halo_pack
+    / fvb_halo_unpack into buffers allocated once."""
 
-    def reduce_and_finalize(post: int):
-        ctx.check(ctx.lib.fvb_run_export(ctx.h, N.C.c_void_p(red.data_ptr())))
-        if cpu_comm:
-            host = red.cpu()
-            dist.all_reduce(host, op=dist.ReduceOp.MAX, group=group)
-            red.copy_(host)
-        else:
-            dist.all_reduce(red, op=dist.ReduceOp.MAX, group=group)
-        ctx.check(ctx.lib.fvb_run_finalize(ctx.h, N.C.c_void_p(red.data_ptr()), post))
+    def __init__(self, ctx, scheme, layout, grid, ncomp, split, cpu_comm):
+        import torch
 
-    def movers(u):
+        self.ctx, self.s, self.L = ctx, scheme, layout
+        self.grid, self.ncomp, self.cpu = grid, ncomp, cpu_comm
+        self.march = grid.dim - 1
+        g = grid.ghost_width
+        self.g = g
+        n = grid.cells[self.march]
+        self.direct = (not cpu_comm) and self.march in split and n >= g
+        self.bufs = {}
+        for axis in split:
+            if self.direct and axis == self.march:
+                continue
+            cnt = int(ctx.lib.fvb_halo_count(N.C.byref(scheme), axis))
+            dev = "cpu" if cpu_comm else "cuda"
+            for side in (0, 1):
+                self.bufs[(axis, side, "send")] = torch.empty(cnt, dtype=torch.float64, device="cuda")
+                self.bufs[(axis, side, "recv")] = torch.empty(cnt, dtype=torch.float64, device=dev,
+                                                              pin_memory=cpu_comm)
+                if cpu_comm:
+                    self.bufs[(axis, side, "host_send")] = torch.empty(cnt, dtype=torch.float64, pin_memory=True)
+
+    def _slab(self, u, side, ghost):
+        """Per-component contiguous views of the march-axis layers: the g
+        interior layers next to face `side` (ghost=False) or its g ghosts."""
+        g, n = self.g, self.grid.cells[self.march]
+        lo = (g if side == 0 else n) if not ghost else (0 if side == 0 else n + g)
+        return [u[0, c, lo:lo + g] for c in range(self.ncomp)]
+
+    def movers(self, u):
+        ctx, s, L = self.ctx, self.s, self.L
         ptr = N.C.c_void_p(u.data_ptr())
 
-        def alloc(axis):
-            cnt = int(ctx.lib.fvb_halo_count(N.C.byref(s), axis))
-            return torch.empty(cnt, dtype=torch.float64, device="cpu" if cpu_comm else u.device)
-
         def pack(axis, side):
-            cnt = int(ctx.lib.fvb_halo_count(N.C.byref(s), axis))
-            buf = torch.empty(cnt, dtype=torch.float64, device=u.device)
+            if self.direct and axis == self.march:
+                return self._slab(u, side, ghost=False)
+            buf = self.bufs[(axis, side, "send")]
             ctx.check(ctx.lib.fvb_halo_pack(ctx.h, N.C.byref(s), N.C.byref(L), ptr, axis, side,
                                             N.C.c_void_p(buf.data_ptr())))
-            return buf.cpu() if cpu_comm else buf
+            if self.cpu:
+                host = self.bufs[(axis, side, "host_send")]
+                host.copy_(buf)
+                return host
+            return buf
+
+        def alloc(axis, side):
+            if self.direct and axis == self.march:
+                return self._slab(u, side, ghost=True)  # received straight into the ghost layers
+            return self.bufs[(axis, side, "recv")]
 
         def unpack(axis, side, buf):
-            b = buf.to(u.device) if cpu_comm else buf
+            if self.direct and axis == self.march:
+                return
+            b = buf.to("cuda", non_blocking=False) if self.cpu else buf
             ctx.check(ctx.lib.fvb_halo_unpack(ctx.h, N.C.byref(s), N.C.byref(L), ptr, axis, side,
                                               N.C.c_void_p(b.data_ptr())))
 
         return pack, unpack, alloc
 
-    def outflow_edges(u, axes):
+
+class DecomposedRun:
+    """The per-rank loop of run_parallel (parallel.py:479-521) for one
+    subdomain on this process's GPU, device resident.
+
+    ``local`` is this rank's subdomain (a host ``Field`` or a ``DeviceField``
+    with its own GridSpec, ghosts included).  Every stage: halo exchange of
+    the stage input over torch.distributed P2P (NCCL; march-axis layers in
+    place, other axes packed into persistent buffers), then the fused stage
+    kernel -- with ``overlap`` and a split march axis, the inner rows [g,
+    n-g) run while the halos are in flight and the two shell slabs after
+    they land (overlapped_residual, parallel.py:325-361).  Every step: one
+    all-reduce(MAX) of [maxima, error flags] and a device finalisation that
+    all ranks evaluate identically (global dt, parallel.py:498-501).  All of
+    it is stream ordered on the run's own stream: the host reads the device
+    state only every ``poll_every`` steps and at the end.  ``cpu_comm``
+    stages the exchanged slabs and the reduce through host memory (gloo),
+    e.g. to test several ranks on one GPU.
+
+    ``advance(n)`` enqueues up to n more steps; ``finish()`` returns
+    (DeviceField of the final subdomain, [RankRecord])."""
+
+    def __init__(self, local, cfg, topo: RankTopology, n_steps=None, *, arith=None, group=None,
+                 cpu_comm: bool = False, overlap: bool = True, poll_every: int = 64, log: bool = True):
+        import torch
+        import torch.distributed as dist
+
+        self.dist, self.group, self.cfg, self.topo = dist, group, cfg, topo
+        self.rank = dist.get_rank(group)
+        self.n_steps = n_steps
+        self.poll_every = max(1, int(poll_every))
+        self.stream = torch.cuda.Stream()
+        with torch.cuda.stream(self.stream):  # NCCL orders after the library's kernels on this stream
+            dev = local if isinstance(local, DeviceField) else DeviceField.from_host(local)
+            self.grid, self.ncomp = dev.grid, dev.ncomp
+            grid = self.grid
+            b0 = dev.data.unsqueeze(0).contiguous()
+            self.bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
+            self.ctx = ctx = N.context()
+            self.split = tuple(k for k in range(grid.dim) if topo.ranks_per_axis[k] > 1)
+            self.periodic = [int(_v(cfg.bc[k]) == "periodic") for k in range(grid.dim)]
+            ctx.check(ctx.lib.fvb_run_set_external_reduce(ctx.h, 1))
+            mode = N.MODE_FIXED if n_steps is not None else N.MODE_PAR_T_END
+            self.run = DeviceRun(grid, cfg, self.bufs, 1, mode, n_steps, arith, halo_axes=self.split, ctx=ctx,
+                                 log=log)
+            self.halos = _Halos(ctx, self.run.scheme, self.run.layout, grid, self.ncomp, self.split, cpu_comm)
+            self.cpu_comm = cpu_comm
+            self.red = torch.zeros(grid.dim + 2, dtype=torch.float64, device="cuda")
+            self.red_host = torch.zeros(grid.dim + 2, dtype=torch.float64, pin_memory=True) if cpu_comm else None
+            self.march = grid.dim - 1
+            self.g = grid.ghost_width
+            self.n_march = grid.cells[self.march] if grid.dim >= 2 else 0
+            self.ovl = overlap and grid.dim >= 2 and self.march in self.split and self.n_march > 2 * self.g
+            self.other = [a for a in self.split if a != self.march]
+            self.nst = 1 if cfg.rk_order == 1 else cfg.rk_order
+            self.steps = 0
+            self.done = False
+            self._tic = time.perf_counter()
+            self._last = 0
+            self._reduce_and_finalize(0)
+
+    def _reduce_and_finalize(self, post: int):
+        ctx, dist, red = self.ctx, self.dist, self.red
+        ctx.check(ctx.lib.fvb_run_export(ctx.h, N.C.c_void_p(red.data_ptr())))
+        if self.cpu_comm:
+            self.red_host.copy_(red)
+            dist.all_reduce(self.red_host, op=dist.ReduceOp.MAX, group=self.group)
+            red.copy_(self.red_host)
+        else:
+            dist.all_reduce(red, op=dist.ReduceOp.MAX, group=self.group)
+        ctx.check(ctx.lib.fvb_run_finalize(ctx.h, N.C.c_void_p(red.data_ptr()), post))
+
+    def _outflow_edges(self, u, axes):
         # world edges of split, non-periodic axes: outflow ghosts (parallel.py:246-247)
-        view = DeviceField(grid, ncomp, u[0])
+        view = DeviceField(self.grid, self.ncomp, u[0])
         for axis in axes:
             for side in (0, 1):
-                if topo.neighbor(rank, axis, side, bool(periodic[axis])) is None:
+                if self.topo.neighbor(self.rank, axis, side, bool(self.periodic[axis])) is None:
                     _fill_one_side(view, axis, side)
 
-    march = grid.dim - 1
-    g = grid.ghost_width
-    n_march = grid.cells[march] if grid.dim >= 2 else 0
-    # overlap schedule (overlapped_residual, parallel.py:325-361): the
-    # march-axis halos travel while the inner box [g, n-g) is computed
-    ovl = overlap and grid.dim >= 2 and march in split and n_march > 2 * g
-
-    def stage(st, u):
-        pack, unpack, alloc = movers(u)
-        if not ovl:
-            halo_exchange_dist(topo, rank, periodic, pack, unpack, alloc, dist, group)
-            outflow_edges(u, split)
+    def _stage(self, st, u):
+        ctx, dist, topo, rank, per, grp = self.ctx, self.dist, self.topo, self.rank, self.periodic, self.group
+        pack, unpack, alloc = self.halos.movers(u)
+        if not self.ovl:
+            halo_exchange_dist(topo, rank, per, pack, unpack, alloc, dist, grp)
+            self._outflow_edges(u, self.split)
             ctx.check(ctx.lib.fvb_run_stage(ctx.h, st))
             return
-        other = [a for a in split if a != march]
-        if other:
-            halo_exchange_dist(topo, rank, periodic, pack, unpack, alloc, dist, group, axes=other)
-            outflow_edges(u, other)
-        handle = start_halo_exchange(topo, rank, periodic, pack, alloc, dist, group, axes=[march])
-        ctx.check(ctx.lib.fvb_run_stage_rows(ctx.h, st, g, n_march - g, 0))      # inner box
+        if self.other:
+            halo_exchange_dist(topo, rank, per, pack, unpack, alloc, dist, grp, axes=self.other)
+            self._outflow_edges(u, self.other)
+        g, n = self.g, self.n_march
+        handle = start_halo_exchange(topo, rank, per, pack, alloc, dist, grp, axes=[self.march])
+        ctx.check(ctx.lib.fvb_run_stage_rows(ctx.h, st, g, n - g, 0))      # inner box
         finish_halo_exchange(handle, unpack)
-        outflow_edges(u, [march])
-        ctx.check(ctx.lib.fvb_run_stage_rows(ctx.h, st, 0, g, 0))                # shell slabs
-        ctx.check(ctx.lib.fvb_run_stage_rows(ctx.h, st, n_march - g, n_march, 1))
+        self._outflow_edges(u, [self.march])
+        ctx.check(ctx.lib.fvb_run_stage_rows(ctx.h, st, 0, g, 0))          # shell slabs
+        ctx.check(ctx.lib.fvb_run_stage_rows(ctx.h, st, n - g, n, 1))
 
-    reduce_and_finalize(0)
-    nst = 1 if cfg.rk_order == 1 else cfg.rk_order
-    while True:
-        infos, done = run.poll()
-        if done[0]:
-            break
-        tic = time.perf_counter()
-        for st in range(nst):
-            stage(st, bufs[int(infos[0].steps) % 2] if nst == 1 else bufs[st])
-        reduce_and_finalize(1)
-        infos, _ = run.poll()
-        run.read_log(infos, time.perf_counter() - tic)
-    info = run.end()[0]
-    if info.err:
-        try:
-            _raise_run_error(info, grid, ncomp)
-        except E.ConslawError as exc:
-            raise E.SimulationError(f"rank {rank} failed: {exc}") from exc
-    final = bufs[int(info.steps) % 2] if cfg.rk_order == 1 else bufs[0]
-    mine = DeviceField(grid, ncomp, final[0]).to_host()
-    recs = [RankRecord(r.step, r.t, r.dt, r.seconds) for r in run.records[0]]
-    # gather the subdomains and the per-rank records (the reference returns all)
-    gathered = [None] * topo.size
-    dist.all_gather_object(gathered, (mine.data, recs), group=group)
-    locs = [Field(parts[r].grid, ncomp, gathered[r][0]) for r in range(topo.size)]
-    return stitch_fields(init.grid, parts, locs), [gathered[r][1] for r in range(topo.size)]
+    def _poll(self):
+        infos, done = self.run.poll()
+        self.run.read_log(infos, (time.perf_counter() - self._tic) / max(1, self.steps - self._last))
+        self._tic, self._last = time.perf_counter(), self.steps
+        self.done = self.done or done[0]
+        return infos
+
+    def advance(self, n: int | None = None) -> int:
+        """Enqueue up to ``n`` more steps (None: to the end); returns how
+        many were enqueued."""
+        import torch
+
+        k = 0
+        with torch.cuda.stream(self.stream):
+            while not self.done and (n is None or k < n):
+                if self.n_steps is not None and self.steps >= self.n_steps:
+                    break
+                if self.steps % self.poll_every == 0 and self.steps > self._last:
+                    self._poll()  # (the step log ring holds 4096 entries)
+                    if self.done:
+                        break
+                elif self.steps == 0 and self.n_steps is None:
+                    self._poll()
+                    if self.done:
+                        break
+                for st in range(self.nst):
+                    self._stage(st, self.bufs[self.steps % 2] if self.nst == 1 else self.bufs[st])
+                self._reduce_and_finalize(1)
+                self.steps += 1
+                k += 1
+        return k
+
+    def finish(self):
+        import torch
+
+        with torch.cuda.stream(self.stream):
+            if self.n_steps is None:
+                self.advance()
+            info = self._poll()[0]
+            info = self.run.end()[0]
+            if info.err:
+                try:
+                    _raise_run_error(info, self.grid, self.ncomp)
+                except E.ConslawError as exc:
+                    raise E.SimulationError(f"rank {self.rank} failed: {exc}") from exc
+            final = self.bufs[int(info.steps) % 2] if self.cfg.rk_order == 1 else self.bufs[0]
+            recs = [RankRecord(r.step, r.t, r.dt, r.seconds) for r in self.run.records[0]]
+            out = DeviceField(self.grid, self.ncomp, final[0])
+        torch.cuda.current_stream().wait_stream(self.stream)
+        return out, recs
+
+
+def run_decomposed(local, cfg, topo: RankTopology, n_steps=None, *, arith=None, group=None,
+                   cpu_comm: bool = False, overlap: bool = True, poll_every: int = 64):
+    """Run one rank's subdomain to the end (see DecomposedRun); returns
+    (DeviceField of the final subdomain, [RankRecord])."""
+    r = DecomposedRun(local, cfg, topo, n_steps, arith=arith, group=group, cpu_comm=cpu_comm, overlap=overlap,
+                      poll_every=poll_every)
+    r.advance()
+    return r.finish()
+
+
+def run_parallel_nccl(init, cfg, topo, parts, n_steps, *, arith=None, group=None, cpu_comm: bool = False,
+                      overlap: bool = True):
+    """One subdomain per process (rank r of the torch.distributed group owns
+    part r): ``run_decomposed`` on the scattered subdomain, then the
+    subdomains travel to rank 0 one at a time (device send/recv, one D2H
+    each) and are stitched there; every rank gets all ranks' records.
+
+    Rank 0 returns the stitched global Field; the other ranks return their
+    own final subdomain (a process-per-GPU caller has no single owner of the
+    global result)."""
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    local = scatter_field(init, [parts[rank]])[0]
+    dev, recs = run_decomposed(local, cfg, topo, n_steps, arith=arith, group=group, cpu_comm=cpu_comm,
+                               overlap=overlap)
+    mine = dev.to_host()
+    allrecs = [None] * world
+    dist.all_gather_object(allrecs, recs, group=group)
+    if world == 1:
+        return stitch_fields(init.grid, parts, [mine]), allrecs
+    if rank == 0:
+        locs = [mine]
+        buf = torch.empty(tuple(mine.data.shape), dtype=torch.float64, device="cpu" if cpu_comm else "cuda")
+        for r in range(1, world):
+            dist.recv(buf, src=r, group=group)
+            locs.append(Field(parts[r].grid, init.ncomp, buf.cpu().numpy().copy()))
+        return stitch_fields(init.grid, parts, locs), allrecs
+    dist.send(torch.from_numpy(np.ascontiguousarray(mine.data)) if cpu_comm else dev.data.contiguous(),
+              dst=0, group=group)
+    return mine, allrecs
 
 
 # ---------------------------------------------------------------------------

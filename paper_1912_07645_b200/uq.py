@@ -392,12 +392,16 @@ def default_batch(grid, ncomp: int) -> int:
 
 
 def run_mc(plan, grid, cfg, evaluate_init, functionals, workers: int = 1, *, batch: int | None = None,
-           arith: str | None = None, group=None):
+           arith: str | None = None, group=None, max_steps: int | None = None):
     """Single-level estimate (uq.py:302-322) on the GPU.
 
-    ``workers`` is accepted for API compatibility (the GPU batch replaces the
-    thread pool).  Under an initialised torch.distributed group the samples
-    are sharded over the ranks and every rank returns the merged result.
+    ``workers`` sizes the host pool that evaluates a host ``evaluate_init``
+    a batch ahead (the GPU batch replaces the reference's per-sample thread
+    pool).  Under an initialised torch.distributed group the samples are
+    sharded over the ranks (contiguous blocks) and every rank returns the
+    merged result.  ``max_steps`` caps the steps of every sample
+    (run_simulation's max_steps, solver.py:199-246) -- bench.py uses it for
+    fixed-work timing.
     """
     import torch
 
@@ -410,7 +414,7 @@ def run_mc(plan, grid, cfg, evaluate_init, functionals, workers: int = 1, *, bat
         world, rank = dist.get_world_size(group), dist.get_rank(group)
     lo, hi = shard_range(plan.samples, world, rank)
     slots = [_Slot(f, grid, ncomp) for f in functionals]
-    _ensemble(plan, 0, grid, cfg, evaluate_init, slots, lo, hi, batch, arith, workers)
+    _ensemble(plan, 0, grid, cfg, evaluate_init, slots, lo, hi, batch, arith, workers, max_steps)
     if dist is not None and world > 1:
         _merge_ranks(slots, dist, group, world)
     return [s.result() for s in slots]
@@ -451,7 +455,8 @@ def _pinned_stage(key):
         return buf
 
 
-def _ensemble(plan, level, grid, cfg, evaluate_init, slots, lo, hi, batch=None, arith=None, workers=1):
+def _ensemble(plan, level, grid, cfg, evaluate_init, slots, lo, hi, batch=None, arith=None, workers=1,
+              max_steps=None):
     """Samples [lo, hi) of one level: batched device runs (one instance per
     sample), each final field pushed into every slot in sample order.
 
@@ -520,13 +525,16 @@ def _ensemble(plan, level, grid, cfg, evaluate_init, slots, lo, hi, batch=None, 
                 b0 = host.to("cuda", non_blocking=True)
                 nxt = pool.submit(prepare, batches[b + 1], (b + 1) % 2) if b + 1 < len(batches) else None
             bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
-            run = DeviceRun(grid, cfg, bufs, len(ks), N.MODE_T_END, None, arith, log=False, ctx=ctx)
+            run = DeviceRun(grid, cfg, bufs, len(ks), N.MODE_T_END, max_steps, arith, log=False, ctx=ctx)
             while True:
                 infos, done = run.poll()
                 if all(done):
                     break
                 left = max(((cfg.t_end - i.t) / i.dt) if (i.dt > 0 and not d) else 1 for i, d in zip(infos, done))
-                run.steps(int(min(512, max(1, math.ceil(left) + 2))))
+                n = min(512, max(1, math.ceil(left) + 2))
+                if max_steps is not None:  # no launches past the cap (they would be no-ops)
+                    n = min(n, max(1, int(max_steps) - min(int(i.steps) for i, d in zip(infos, done) if not d)))
+                run.steps(int(n))
             infos = run.end()
             for j, info in zip(ks, infos):
                 if info.err:

@@ -69,7 +69,7 @@ def test_rank_ordered_moment_merge_gloo():
     assert out[0] and out[1]
 
 
-def _halo_worker(rank, world, port, lay, periodic, out):
+def _halo_worker(rank, world, port, lay, periodic, out, listy=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -97,14 +97,19 @@ def _halo_worker(rank, world, port, lay, periodic, out):
 
     def pack(axis, side):
         n = loc_cells[axis]
-        return torch.from_numpy(np.ascontiguousarray(u[sl(axis, g, 2 * g) if side == 0 else sl(axis, n, n + g)]))
+        slab = np.ascontiguousarray(u[sl(axis, g, 2 * g) if side == 0 else sl(axis, n, n + g)])
+        if listy and axis == 1:  # march axis: one contiguous message per component (parallel._Halos)
+            return [torch.from_numpy(np.ascontiguousarray(slab[c])) for c in range(slab.shape[0])]
+        return torch.from_numpy(slab)
 
-    def alloc(axis):
-        return torch.empty_like(pack(axis, 0))
+    def alloc(axis, side):
+        b = pack(axis, 0)
+        return [torch.empty_like(x) for x in b] if isinstance(b, list) else torch.empty_like(b)
 
     def unpack(axis, side, buf):
         n = loc_cells[axis]
-        u[sl(axis, 0, g) if side == 0 else sl(axis, n + g, n + 2 * g)] = buf.numpy()
+        val = np.stack([x.numpy() for x in buf]) if isinstance(buf, list) else buf.numpy()
+        u[sl(axis, 0, g) if side == 0 else sl(axis, n + g, n + 2 * g)] = val
 
     PP.halo_exchange_dist(topo, rank, periodic, pack, unpack, alloc, dist)
     ok = True
@@ -128,13 +133,14 @@ def _halo_worker(rank, world, port, lay, periodic, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("lay,periodic", [((2, 1), (True, True)), ((2, 2), (True, True)), ((2, 2), (False, True)),
-                                          ((1, 2), (True, False))])
-def test_halo_exchange_dist_gloo(lay, periodic):
+@pytest.mark.parametrize("lay,periodic,listy", [((2, 1), (True, True), False), ((2, 2), (True, True), False),
+                                                ((2, 2), (False, True), False), ((1, 2), (True, False), False),
+                                                ((1, 2), (True, True), True), ((2, 2), (True, False), True)])
+def test_halo_exchange_dist_gloo(lay, periodic, listy):
     world = lay[0] * lay[1]
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_halo_worker, args=(world, _free_port(), lay, periodic, out), nprocs=world, join=True)
+    mp.spawn(_halo_worker, args=(world, _free_port(), lay, periodic, out, listy), nprocs=world, join=True)
     assert all(out[r] for r in range(world))
 
 
