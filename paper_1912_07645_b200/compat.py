@@ -13,6 +13,7 @@ from __future__ import annotations
 import importlib
 
 from . import errors as E
+from . import numerics as _num
 from . import parallel as _par
 from . import solver as _sol
 from . import uq as _uq
@@ -22,7 +23,7 @@ def install_into(pkg) -> dict:
     """Rebind the hot-path entry points of an imported ``conslaw`` package.
     Returns {qualified name: previous object} so callers can undo."""
     mods = {name: importlib.import_module(f"{pkg.__name__}.{name}")
-            for name in ("solver", "uq", "parallel", "cli", "errors", "grid")}
+            for name in ("solver", "uq", "parallel", "cli", "errors", "grid", "numerics")}
     saved = {}
 
     def bind(mod, attr, new):
@@ -44,6 +45,16 @@ def install_into(pkg) -> dict:
     for m in (mods["uq"], mods["cli"]):
         bind(m, "run_mc", _uq.run_mc)
         bind(m, "run_mlmc", _uq.run_mlmc)
+    # the numerics function API and the flux registry seam (numerics.py:64-210):
+    # device implementations, keyed by the reference's own FluxKind members
+    nm = mods["numerics"]
+    for attr in ("weno_weights", "weno_face_value", "reconstruct_axis", "reconstruct", "rusanov_flux",
+                 "hllc_flux", "numerical_flux"):
+        bind(nm, attr, getattr(_num, attr))
+    if hasattr(nm, "FLUX_FUNCTIONS") and hasattr(nm, "FluxKind"):
+        saved[f"{nm.__name__}.FLUX_FUNCTIONS"] = dict(nm.FLUX_FUNCTIONS)
+        nm.FLUX_FUNCTIONS[nm.FluxKind.RUSANOV] = _num.rusanov_flux
+        nm.FLUX_FUNCTIONS[nm.FluxKind.HLLC] = _num.hllc_flux
     # result / error classes of the reference
     _sol.TYPES["TimeStepRecord"] = mods["solver"].TimeStepRecord
     _sol.TYPES["Field"] = mods["grid"].Field

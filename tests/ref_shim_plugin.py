@@ -1,0 +1,19 @@
+"""pytest plugin (``-p tests.ref_shim_plugin``) that routes the reference
+package's hot path to the B200 implementation before the reference's own
+test modules are imported: compat.install_into(conslaw) rebinds every
+import-time binding (solver, uq, parallel, cli, numerics, error classes).
+Used by tests/test_gpu_reference_suite.py on the reference's own test suite
+(baseline/_ref/conslaw_tests, placed there by tools/vendor_reference.sh)."""
+
+
+def pytest_configure(config):
+    import conslaw
+
+    from paper_1912_07645_b200.compat import install_into
+
+    install_into(conslaw)
+    config._fvb_shim = True
+
+
+def pytest_report_header(config):
+    return "conslaw hot path -> paper_1912_07645_b200 (compat.install_into)"
