@@ -212,26 +212,34 @@ __global__ void __launch_bounds__(kSfThreads) structure_pass1(Pad p, fvb_layout 
   }
 }
 
-// Pass 2 (one block): fixed-order sum of the partials, then the reference's
-// accumulation  acc = sum_j mean_j ; sums[h] += acc / dim  (uq.py:257-261).
-__global__ void structure_pass2(const double* __restrict__ partials, int nblocks, int H, int dim, double ncell, double* sums) {
-  __shared__ double red[kSfThreads];
-  for (int h = 0; h <= H; ++h) {  // any max offset: no per-(h, j) table
-    double accj = 0.0;           // thread 0: sum_j mean_j, in j order
-    for (int j = 0; j < dim; ++j) {
-      const int hj = h * dim + j;
+// Pass 2 (one block): fixed-order sum of the partials -- one warp per
+// (offset h, numpy axis j) pair, lane-strided over the blocks then a
+// shuffle tree -- and the reference's accumulation acc = sum_j mean_j ;
+// sums[h] += acc / dim (uq.py:257-261).  Offsets go in chunks of 8, so any
+// max offset works with a fixed-size table.
+__global__ void structure_pass2(const double* __restrict__ partials, int nblocks, int H, int dim, double ncell,
+                                double* sums) {
+  __shared__ double S[8 * 3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int hb = 0; hb <= H; hb += 8) {
+    for (int k = warp; k < 8 * dim; k += nwarps) {
+      const int h = hb + k / dim, j = k % dim;
+      if (h > H) continue;
       double acc = 0.0;
-      for (int b = threadIdx.x; b < nblocks; b += blockDim.x) acc += partials[(int64_t)b * (H + 1) * dim + hj];
-      red[threadIdx.x] = acc;
-      __syncthreads();
-      for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-        __syncthreads();
-      }
-      if (threadIdx.x == 0) accj += red[0] / ncell;
-      __syncthreads();
+      for (int b = lane; b < nblocks; b += 32) acc += partials[((int64_t)b * (H + 1) + h) * dim + j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+      if (lane == 0) S[k] = acc;
     }
-    if (threadIdx.x == 0) sums[h] += accj / dim;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int h = hb; h <= H && h < hb + 8; ++h) {
+        double accj = 0.0;
+        for (int j = 0; j < dim; ++j) accj += S[(h - hb) * dim + j] / ncell;
+        sums[h] += accj / dim;
+      }
+    }
+    __syncthreads();
   }
 }
 

@@ -231,12 +231,16 @@ static int stage_occupancy(const fvb_scheme& s, const StageParams& p) {
 static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t row_lo = 0, int64_t row_hi = -1) {
   int nt, nty;
   const char* kv = getenv("FVB_KERNEL");
-  // 2D default: the cp.async ring kernel (fastest measured);
-  // FVB_KERNEL=tile / strip select the register-window variants
-  p.variant = 2;
+  // 2D default: the cp.async ring kernel; fast-mode Euler runs the pair
+  // kernel (two x-columns per thread).
+  // FVB_KERNEL=ring / pair / tile / strip select explicitly.
+  p.variant = (s.dim == 2 && s.eq == FVB_EQ_EULER && s.arith == FVB_ARITH_FAST) ? 3 : 2;
+  if (kv && std::strcmp(kv, "ring") == 0) p.variant = 2;
   if (kv && std::strcmp(kv, "strip") == 0) p.variant = 0;
   if (kv && std::strcmp(kv, "tile") == 0) p.variant = 1;
-  if (s.dim == 1 && p.variant == 2) p.variant = 1;
+  if (kv && std::strcmp(kv, "pair") == 0) p.variant = 3;
+  if (s.dim == 1 && p.variant >= 2) p.variant = 1;
+  if (p.variant == 3 && (s.dim != 2 || s.eq != FVB_EQ_EULER)) p.variant = 2;  // pair kernel: 2D Euler
   if (s.arith == FVB_ARITH_FAST) fvb::fast::stage_block(s.dim, s.eq, p.variant, nt, nty);
   else fvb::exact::stage_block(s.dim, s.eq, p.variant, nt, nty);
   const int64_t strips = (p.n[0] + (nt - 2) - 1) / (nt - 2);

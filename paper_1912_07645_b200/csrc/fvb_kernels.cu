@@ -33,6 +33,7 @@ constexpr int kRingNT = FVB_RING_NT, kRingNTScalar = FVB_RING_NT_SCALAR;
 void stage_block(int dim, int eq, int variant, int& nt, int& nty) {
   if (dim == 1 && variant == 2) variant = 1;
   if (dim == 2 && variant == 2) { nt = eq == EQ_EULER ? kRingNT : kRingNTScalar; nty = 1; return; }
+  if (dim == 2 && variant == 3) { nt = 2 * kPairNT; nty = 1; return; }  // 62 cells per one-warp block
   if (dim == 3 && variant == 2) { nt = kRing3NT; nty = kRing3NTY; return; }
   if (dim <= 2 && variant == 0) { nt = kStripCells * kStripWarps + 2; nty = 1; }
   else if (dim == 1) { nt = Blk<1>::NT; nty = 1; }
@@ -109,6 +110,12 @@ static int launch_ring(const StageParams& p, dim3 grid, cudaStream_t s) {
   return launch_pdl(ring_kernel<EQ, FLUX, RECON, NT, KS, FIN>, grid, dim3(NT), smem, s, p);
 }
 
+template <int EQ, int FLUX, int RECON, int KS, bool FIN>
+static int launch_pair(const StageParams& p, dim3 grid, cudaStream_t s) {
+  const int smem = pair_smem_bytes<EQ>() + 4 * (p.H + kRingPD + 4);
+  return launch_pdl(pair_kernel<EQ, FLUX, RECON, KS, FIN>, grid, dim3(kPairNT), smem, s, p);
+}
+
 template <int DIM, int EQ, int FLUX, int RECON, bool FIN>
 static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
   if constexpr (DIM == 3) {
@@ -120,6 +127,15 @@ static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
       if (grid.x == 0) return occupancy(kern, dim3(kRing3NT, kRing3NTY), smem);
       kern<<<grid, dim3(kRing3NT, kRing3NTY), smem, s>>>(p);
       return 0;
+    }
+  }
+  if constexpr (DIM == 2 && EQ == EQ_EULER) {
+    if (p.variant == 3) {  // two x-columns per thread (Euler)
+      const int ks = p.kind == 0 ? 0 : (p.kind == 1 ? 1 : 2);
+      if (FIN && ks == 0) return -1;
+      if (ks == 0) return launch_pair<EQ, FLUX, RECON, (FIN ? 1 : 0), FIN>(p, grid, s);
+      if (ks == 1) return launch_pair<EQ, FLUX, RECON, 1, FIN>(p, grid, s);
+      return launch_pair<EQ, FLUX, RECON, 2, FIN>(p, grid, s);
     }
   }
   if constexpr (DIM == 2) {

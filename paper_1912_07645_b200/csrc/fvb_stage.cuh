@@ -1188,6 +1188,283 @@ constexpr int ring_smem_bytes() {
 }
 
 // ---------------------------------------------------------------------------
+// 2D pair kernel: the ring kernel with TWO x-columns per thread.
+//
+// A one-warp block owns 62 x-cells (64 face cells: lane t holds face cells
+// f0 = x0-1+2t and f1 = f0+1, lane 0's f0 and lane 31's f1 are the halo
+// face cells) and marches H rows in y.  Per thread and row: two WENO
+// stencils per axis, the x interface between its own two cells computed
+// in-thread and one more with the neighbour lane's face (shuffle), two y
+// interfaces -- two independent chains of the same physics interleave
+// (ILP 2), and the per-row bookkeeping (ring copies, slot rotation, march
+// recurrence, stores) is shared by two cells: ring rows arrive by 16-byte
+// cp.async (pairs of cells; 8-byte copies where a pair is not contiguous:
+// outflow edges, odd periodic extents), the x stencil and the march
+// recurrence move as 16-byte shared-memory accesses, and a one-warp block
+// synchronises with __syncwarp only.  Same operation order as the ring
+// kernel, so the exact mode stays bitwise.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+
+constexpr int kPairNT = 32;                // one warp
+constexpr int kPairW = 2 * kPairNT + 2;    // ring row width: cells x0-2 .. x0+63
+
+#ifndef FVB_PAIR_MINB
+#define FVB_PAIR_MINB 12  // <= 168 registers: 12 one-warp blocks/SM (measured: 23.5 vs 22.9 at 8, 17.8 at 14 -- spills)
+#endif
+
+template <int EQ, int FLUX, int RECON, int KS, bool FIN>
+__global__ void __launch_bounds__(kPairNT, FVB_PAIR_MINB)
+pair_kernel(const StageParams p) {
+  constexpr int DIM = 2;
+  constexpr int NC = NComp<EQ, DIM>::value;
+  constexpr int W = kPairW;
+  constexpr bool UN = KS == 2;
+  static_assert(!UN || kRingPD == 1, "the 2-slot u^n ring assumes one ring row in flight");
+  extern __shared__ __align__(16) double smem[];
+  double* ring = smem;                          // [kRingRows][NC][W]
+  double* gx = ring + kRingRows * NC * W;       // [NC][64]: x residual of each face cell (own column pair)
+  double* nrow = gx + NC * 64;                  // [NC][64]: u^n of the row finished next
+  double* hs = nrow + NC * 64;                  // [NC][64]: high y face of the previous row
+  double* gs = hs + NC * 64;                    // [NC][64]: y flux below the previous row
+  auto RG = [&](int slot, int c, int x) -> double& { return ring[(slot * NC + c) * W + x]; };
+
+#if FVB_PDL
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#endif
+  const int inst = blockIdx.z;
+  FvbState* st = p.st + (p.shared_state ? 0 : inst);
+  if (*(volatile int*)&st->done) return;
+  const double dt = KS == 0 ? 0.0 : *(volatile double*)&st->dt;
+  const int cs = (int)p.sc;
+  const double* __restrict__ us = p.us + p.origin + inst * p.si;
+  const double* un = p.un + p.origin + inst * p.si;
+  double* out = p.out + p.origin + inst * p.si;
+  const int t = threadIdx.x;
+  const int nx = (int)p.n[0];
+  const int x0 = blockIdx.x * (2 * kPairNT - 2);
+  const int f0 = x0 - 1 + 2 * t;                     // face cells f0, f0+1 of this lane
+  const bool cell0 = t >= 1 && f0 < nx;              // updated cells (lane 0's f0 is the halo face cell)
+  const bool cell1 = t <= kPairNT - 2 && f0 + 1 < nx;
+  const int ra = (int)p.row_lo + blockIdx.y * p.H;
+  const int rb = min(ra + p.H, (int)p.row_hi);
+  const int co0 = (int)map_index(f0, nx, p.bc[0], p.g), co1 = (int)map_index(f0 + 1, nx, p.bc[0], p.g);
+  // ring pair j = cells (x0-2+2j, x0-1+2j): lane t copies pair t, lane 0 also pair 32
+  const int pa = (int)map_index(x0 - 2 + 2 * t, nx, p.bc[0], p.g);
+  const int pb = (int)map_index(x0 - 1 + 2 * t, nx, p.bc[0], p.g);
+  const int qa = (int)map_index(x0 + 62, nx, p.bc[0], p.g), qb = (int)map_index(x0 + 63, nx, p.bc[0], p.g);
+  // 16-byte copies need the pair contiguous and 16-byte aligned in memory
+  const bool vec = ((((int64_t)p.origin + pa) & 1) == 0) && pb == pa + 1 && qb == qa + 1 &&
+                   ((reinterpret_cast<uintptr_t>(p.us) & 15) == 0) && ((p.sy & 1) == 0) && ((cs & 1) == 0);
+  const bool vec_all = __all_sync(0xffffffffu, vec);
+  int* rtab = reinterpret_cast<int*>(gs + NC * 64);
+  for (int i = t; i < p.H + kRingPD + 4; i += kPairNT)
+    rtab[i] = (int)(map_index(ra - 2 + i, p.n[1], p.bc[1], p.g) * p.sy);
+  __syncwarp();
+  auto roff = [&](int r) -> int { return rtab[r - (ra - 2)]; };
+  auto fetch = [&](int r, int slot) {
+    const int ro = roff(r);
+    if (vec_all) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) cp_async16(&RG(slot, c, 2 * t), us + (pa + ro + c * cs));
+      if (t == 0) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) cp_async16(&RG(slot, c, 64), us + (qa + ro + c * cs));
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        cp_async8(&RG(slot, c, 2 * t), us + (pa + ro + c * cs));
+        cp_async8(&RG(slot, c, 2 * t + 1), us + (pb + ro + c * cs));
+      }
+      if (t == 0) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          cp_async8(&RG(slot, c, 64), us + (qa + ro + c * cs));
+          cp_async8(&RG(slot, c, 65), us + (qb + ro + c * cs));
+        }
+      }
+    }
+  };
+
+  unsigned errb = 0;
+  double smax[DIM] = {0.0, 0.0};
+  const double rk_a = p.kind == 2 ? 0.5 : (p.kind == 3 ? 0.75 : (p.kind == 4 ? 1.0 / 3.0 : 0.0));
+  const double rk_b = p.kind == 2 ? 0.5 : (p.kind == 3 ? 0.25 : (p.kind == 4 ? 2.0 / 3.0 : 1.0));
+#if FVB_FAST
+  const double cxs = KS == 0 ? 1.0 : (KS == 1 ? dt : rk_b * dt);  // gx is already scaled by 1/dx
+  const double cy = KS == 0 ? p.id[1] : (KS == 1 ? dt * p.id[1] : rk_b * dt * p.id[1]);
+#endif
+
+  for (int k = 0; k < kRingPD + 2; ++k) {
+    fetch(ra - 2 + k, k);
+    cp_async_commit();
+  }
+  // u^n of row r (finished at iteration r+1) is copied into the single
+  // per-lane slot right after iteration r's finish read it, in its own
+  // commit group -- the next iteration's wait covers it
+  auto fetch_un = [&](int r) {
+    if constexpr (UN) {
+      if (r >= ra && r < rb) {
+        const int o = roff(r);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (cell0) cp_async8(&nrow[c * 64 + 2 * t], un + (co0 + o + c * cs));
+          if (cell1) cp_async8(&nrow[c * 64 + 2 * t + 1], un + (co1 + o + c * cs));
+        }
+      }
+      cp_async_commit();
+    }
+  };
+  int sA = 0;
+  for (int r = ra - 1; r <= rb; ++r) {
+    const int sB = sA + 1 == kRingRows ? 0 : sA + 1;
+    const int sC = sB + 1 == kRingRows ? 0 : sB + 1;
+    if (r == ra) __syncwarp();
+    {
+      int sN = sC + kRingPD;
+      sN = sN >= kRingRows ? sN - kRingRows : sN;
+      if (r + 1 + kRingPD <= rb + 1) fetch(r + 1 + kRingPD, sN);
+      cp_async_commit();
+    }
+    // groups pending: [u^n of row r-1 (UN), ring row r+1+PD]; everything
+    // older -- ring rows up to r+1 and u^n of row r-1 -- must have landed
+    cp_async_wait<kRingPD>();
+    __syncwarp();
+    // row r of this lane's stencil: p0..p3 = cells f0-1, f0, f1, f1+1
+    double P0[NC], P1[NC], P2[NC], P3[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double2 lo2 = *reinterpret_cast<const double2*>(&RG(sB, c, 2 * t));
+      const double2 hi2 = *reinterpret_cast<const double2*>(&RG(sB, c, 2 * t + 2));
+      P0[c] = lo2.x;
+      P1[c] = lo2.y;
+      P2[c] = hi2.x;
+      P3[c] = hi2.y;
+    }
+    {  // march (y): faces of row r, fluxes (r-1|r), finish row r-1 -- both columns
+      double A0[NC], A1[NC], C0[NC], C1[NC], hi0[NC], lo0[NC], hi1[NC], lo1[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        A0[c] = RG(sA, c, 2 * t + 1);
+        A1[c] = RG(sA, c, 2 * t + 2);
+        C0[c] = RG(sC, c, 2 * t + 1);
+        C1[c] = RG(sC, c, 2 * t + 2);
+      }
+      weno_faces_nc<NC, RECON>(A0, P1, C0, p.P.eps, hi0, lo0);
+      weno_faces_nc<NC, RECON>(A1, P2, C1, p.P.eps, hi1, lo1);
+      if (r >= ra) {
+        double H0[NC], H1[NC], G0[NC], G1[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const double2 h = *reinterpret_cast<const double2*>(&hs[c * 64 + 2 * t]);
+          H0[c] = h.x;
+          H1[c] = h.y;
+        }
+        unsigned eb0 = 0, eb1 = 0;
+        interface_flux<EQ, FLUX, DIM, RECON>(H0, lo0, A0, P1, 1, p.P, G0, eb0);
+        interface_flux<EQ, FLUX, DIM, RECON>(H1, lo1, A1, P2, 1, p.P, G1, eb1);
+        if ((eb0 && cell0) || (eb1 && cell1)) errb |= 2u;
+        if (r - 1 >= ra) {
+          double v0[NC], v1[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const double2 gp = *reinterpret_cast<const double2*>(&gs[c * 64 + 2 * t]);
+            const double2 xr = *reinterpret_cast<const double2*>(&gx[c * 64 + 2 * t]);
+            double un0 = 0.0, un1 = 0.0;
+            if constexpr (UN) {
+              const double2 u2 = *reinterpret_cast<const double2*>(&nrow[c * 64 + 2 * t]);
+              un0 = u2.x;
+              un1 = u2.y;
+            }
+#if FVB_FAST
+            double b0 = KS == 0 ? 0.0 : (KS == 1 ? A0[c] : fma(rk_b, A0[c], rk_a * un0));
+            double b1 = KS == 0 ? 0.0 : (KS == 1 ? A1[c] : fma(rk_b, A1[c], rk_a * un1));
+            v0[c] = fma(cy, gp.x - G0[c], fma(cxs, xr.x, b0));
+            v1[c] = fma(cy, gp.y - G1[c], fma(cxs, xr.y, b1));
+#else
+            const double L0 = xr.x - ddiv(G0[c] - gp.x, p, 1);
+            const double L1 = xr.y - ddiv(G1[c] - gp.y, p, 1);
+            v0[c] = KS == 0 ? L0 : rk_combine(p.kind, un0, A0[c], dt, L0);
+            v1[c] = KS == 0 ? L1 : rk_combine(p.kind, un1, A1[c], dt, L1);
+#endif
+          }
+          const int o = roff(r - 1);
+          if (cell0) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) out[co0 + o + c * cs] = v0[c];
+            if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v0, f0, r - 1, 0, smax);
+          }
+          if (cell1) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) out[co1 + o + c * cs] = v1[c];
+            if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v1, f0 + 1, r - 1, 0, smax);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) *reinterpret_cast<double2*>(&gs[c * 64 + 2 * t]) = make_double2(G0[c], G1[c]);
+      }
+      fetch_un(r);  // the slot was read above (row r-1): refill with row r
+#pragma unroll
+      for (int c = 0; c < NC; ++c) *reinterpret_cast<double2*>(&hs[c * 64 + 2 * t]) = make_double2(hi0[c], hi1[c]);
+    }
+    if (r >= ra && r < rb) {  // x direction of row r
+      if constexpr (EQ == EQ_EULER) {
+        if (p.check_input) {
+          const bool bad0 = cell0 && !euler_physical<DIM>(P1, p.P);
+          const bool bad1 = cell1 && !euler_physical<DIM>(P2, p.P);
+          if (bad0 || bad1)
+            atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | flat_cell<DIM>(p, bad0 ? f0 : f0 + 1, r, 0));
+        }
+      }
+      double hi0[NC], lo0[NC], hi1[NC], lo1[NC];
+      weno_faces_nc<NC, RECON>(P0, P1, P2, p.P.eps, hi0, lo0);
+      weno_faces_nc<NC, RECON>(P1, P2, P3, p.P.eps, hi1, lo1);
+      double uLa[NC], Ga[NC], Gb[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) uLa[c] = __shfl_up_sync(0xffffffffu, hi1[c], 1);  // f0-1's high face
+      unsigned eba = 0, ebb = 0;
+      // interface (f0-1 | f0): cells P0, P1; interface (f0 | f1): cells P1, P2 (fallback operands)
+      interface_flux<EQ, FLUX, DIM, RECON>(uLa, lo0, P0, P1, 0, p.P, Ga, eba);
+      interface_flux<EQ, FLUX, DIM, RECON>(hi0, lo1, P1, P2, 0, p.P, Gb, ebb);
+      if ((eba && t >= 1 && f0 <= nx) || (ebb && f0 + 1 <= nx)) errb |= 1u;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double Gc = __shfl_down_sync(0xffffffffu, Ga[c], 1);  // (f1 | f1+1) of the next lane
+#if FVB_FAST
+        *reinterpret_cast<double2*>(&gx[c * 64 + 2 * t]) = make_double2((Ga[c] - Gb[c]) * p.id[0],
+                                                                         (Gb[c] - Gc) * p.id[0]);
+#else
+        *reinterpret_cast<double2*>(&gx[c * 64 + 2 * t]) = make_double2(0.0 - ddiv(Gb[c] - Ga[c], p, 0),
+                                                                         0.0 - ddiv(Gc - Gb[c], p, 0));
+#endif
+      }
+    }
+    sA = sB;
+  }
+  cp_async_wait<0>();
+#if FVB_PDL
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
+  if (errb) {
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+      if (errb & (1u << a))
+        atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | ((long long)(1 + a) << 40));
+  }
+  if constexpr (FIN) block_epilogue<DIM>(p, st, inst, smax, true);
+}
+
+template <int EQ>
+constexpr int pair_smem_bytes() {
+  constexpr int NC = NComp<EQ, 2>::value;
+  return 8 * (kRingRows * NC * kPairW + NC * 64 + NC * 64 + 2 * NC * 64);
+}
+
+// ---------------------------------------------------------------------------
 // 3D ring kernel (variant 2 in 3D): the 2D ring design on an in-plane tile.
 //
 // A block of 32 x 8 threads owns the 30 x 6 interior cells of its (x, y)

@@ -150,6 +150,9 @@ __device__ inline void export_step(const FvbState* st, int dim, double* out) {
 
 __device__ inline void finalize_global(FvbState* st, const LoopCtl& L, const double* g, bool post) {
   volatile FvbState* vs = st;
+  // steps enqueued past the end (the host polls only every few steps) leave
+  // the finished state untouched, like the no-op stage kernels before them
+  if (vs->done) return;
   for (int k = 0; k < L.dim; ++k) vs->smax[k] = (unsigned long long)__double_as_longlong(g[k]);
   const bool local_hard = vs->stage_err != kNone || vs->bad_nonfinite != kNone;
   if (g[L.dim] != 0.0 && !local_hard) {  // another rank failed this step

@@ -43,7 +43,8 @@ def test_euler_flux_bitwise(NM, dim, flux):
     rng = np.random.default_rng(dim * 7 + len(flux))
     uL, uR = _states(rng, dim, 5000), _states(rng, dim, 5000)
     uR[:, ::17] = uL[:, ::17]  # exact consistency F(u, u) = f(u) (numerics.py:195-196)
-    uR[0, 3::29] = uL[0, 3::29]
+    uR[1:, 3::29] = uL[1:, 3::29] * 1.25  # equal momenta/energy ratios, different states
+    uR[0, 3::29] = uL[0, 3::29] * 1.25
     model = P.EquationModel("euler", dim)
     sc = O.Scheme(dim=dim, cells=(4,) * dim, deltas=(0.25,) * dim, eq="euler", flux=flux)
     for axis in range(dim):

@@ -1,0 +1,5 @@
+# full GPU suite incl. the reference's own tests through the shim
+set -x
+mkdir -p gpurun_out
+python -m pytest tests -m gpu -q > gpurun_out/s_tests.txt 2>&1; echo "tests rc=$?" >> gpurun_out/s_tests.txt
+echo done

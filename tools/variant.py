@@ -29,4 +29,6 @@ with cf.ThreadPoolExecutor(len(units)) as ex:
     list(ex.map(lambda u: B._compile((u[0], u[1], u[2] + args), out), units))
 cmd = [B.NVCC] + B.ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", str(out / "libfvb200.so")] + [str(out / u[1]) for u in B.UNITS]
 subprocess.run(cmd, check=True)
+for u in B.UNITS:  # keep only the linked library (gpurun snapshot size)
+    (out / u[1]).unlink(missing_ok=True)
 print(out / "libfvb200.so")
