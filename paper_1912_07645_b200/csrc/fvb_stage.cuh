@@ -1567,7 +1567,17 @@ ring3_kernel(const StageParams p) {
     if (r + 2 <= rb + 1) fetch(r + 2, (sA + 3) & 3);  // into the slot of plane r-2
     cp_async_commit();
     cp_async_wait<1>();  // planes up to r+1 have landed (own copies)
-    __syncthreads();     // ... everybody's
+    __syncthreads();     // ... everybody's; also: plane r-1's y fluxes (gf) are visible
+    if (inrow && r - 1 >= ra && r - 1 < rb) {  // plane r-1's y residual, deferred past this barrier
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+#if FVB_FAST
+        R[c] = fma(gf[FI(c, ty, tx)] - gf[FI(c, ty + 1, tx)], p.id[1], R[c]);
+#else
+        R[c] = R[c] - ddiv(gf[FI(c, ty + 1, tx)] - gf[FI(c, ty, tx)], p, 1);
+#endif
+      }
+    }
     if (inrow) {  // z: faces of plane r, flux (r-1|r), finish plane r-1 (own column)
       double A[NC], B[NC], C[NC], hi[NC], lo[NC];
 #pragma unroll
@@ -1707,18 +1717,9 @@ ring3_kernel(const StageParams p) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) gf[FI(c, ty, tx)] = G[c];
       }
-      __syncthreads();
-      if (inrow) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-#if FVB_FAST
-          R[c] = fma(gf[FI(c, ty, tx)] - gf[FI(c, ty + 1, tx)], p.id[1], R[c]);
-#else
-          R[c] = R[c] - ddiv(gf[FI(c, ty + 1, tx)] - gf[FI(c, ty, tx)], p, 1);
-#endif
-        }
-      }
-      // gf / hf / lf are rewritten only after the next iteration's top barrier
+      // the y residual of this plane is added after the next iteration's top
+      // barrier (one barrier per plane fewer); gf / hf / lf are rewritten only
+      // after the next iteration's mid barrier
     }
     sA = sB;
   }
