@@ -236,6 +236,8 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
   // FVB_KERNEL=ring / pair / tile / strip select explicitly.
   p.variant = (s.dim == 2 && s.eq == FVB_EQ_EULER && s.arith == FVB_ARITH_FAST) ? 3 : 2;
   if (kv && std::strcmp(kv, "ring") == 0) p.variant = 2;
+  if (s.dim == 3 && p.variant == 2) p.variant = 4;  // 3D default: all-interior-rows ring kernel
+  if (kv && std::strcmp(kv, "ring3") == 0) p.variant = 2;
   if (kv && std::strcmp(kv, "strip") == 0) p.variant = 0;
   if (kv && std::strcmp(kv, "tile") == 0) p.variant = 1;
   if (kv && std::strcmp(kv, "pair") == 0) p.variant = 3;

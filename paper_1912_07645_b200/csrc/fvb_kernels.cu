@@ -35,6 +35,7 @@ void stage_block(int dim, int eq, int variant, int& nt, int& nty) {
   if (dim == 2 && variant == 2) { nt = eq == EQ_EULER ? kRingNT : kRingNTScalar; nty = 1; return; }
   if (dim == 2 && variant == 3) { nt = 2 * kPairNT; nty = 1; return; }  // 62 cells per one-warp block
   if (dim == 3 && variant == 2) { nt = kRing3NT; nty = kRing3NTY; return; }
+  if (dim == 3 && variant == 4) { nt = kR3iNT; nty = kR3iNTY + 2; return; }  // 30 x 8 cells per block
   if (dim <= 2 && variant == 0) { nt = kStripCells * kStripWarps + 2; nty = 1; }
   else if (dim == 1) { nt = Blk<1>::NT; nty = 1; }
   else if (dim == 2) { nt = Blk<2>::NT; nty = 1; }
@@ -119,6 +120,15 @@ static int launch_pair(const StageParams& p, dim3 grid, cudaStream_t s) {
 template <int DIM, int EQ, int FLUX, int RECON, bool FIN>
 static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
   if constexpr (DIM == 3) {
+    if (p.variant == 4) {  // all-interior rows (default 3D)
+      const int smem = ring3i_smem_bytes<EQ>() + 4 * (p.H + 4);  // + plane-offset table
+      auto kern = ring3i_kernel<EQ, FLUX, RECON, FIN>;
+      static unsigned done = 0;  // per instantiation
+      ensure_smem(kern, 227 * 1024, done);
+      if (grid.x == 0) return occupancy(kern, dim3(kR3iNT, kR3iNTY), smem);
+      kern<<<grid, dim3(kR3iNT, kR3iNTY), smem, s>>>(p);
+      return 0;
+    }
     if (p.variant == 2) {
       const int smem = ring3_smem_bytes<EQ>() + 8 * (p.H + 4);  // + plane-offset table
       auto kern = ring3_kernel<EQ, FLUX, RECON, FIN>;

@@ -1739,6 +1739,307 @@ constexpr int ring3_smem_bytes() {
   return 8 * (kRing3Slots * NC * (kRing3NTY + 2) * (kRing3NT + 2) + 5 * NC * kRing3NTY * kRing3NT);
 }
 
+// ---------------------------------------------------------------------------
+// 3D ring kernel, all-interior rows (variant 4, default 3D).
+//
+// A block of 32 x 8 threads owns a 30 x 8 cell tile: warp ty is cell row
+// y0+ty (every warp updates cells; lanes 0 / 31 are the x-halo face cells)
+// and marches H planes along z.  The tile's y-halo work -- the high face of
+// row -1 and the low face of row 8 -- is two extra WENO passes (warps 0 and
+// 7), and the extra interface (7|8) is computed by warp 7; a plane ring of 12
+// rows (y0-2 .. y0+9) x 34 columns streams in by cp.async one plane ahead.
+// z and x sweeps read only the thread's own warp's copies; the y sweep goes
+// through one face and one flux buffer with two block barriers per plane
+// (the y residual of a plane is added after the next plane's top barrier).
+// Compared with ring3_kernel (30 x 6 cells, rows 0 and 7 halo warps idle
+// through the z and x sweeps) every warp has z/x work and a block carries
+// 33 % more cells for the same two barriers.
+// ---------------------------------------------------------------------------
+constexpr int kR3iNT = 32, kR3iNTY = 8, kR3iRows = kR3iNTY + 4, kR3iW = kR3iNT + 2;
+
+template <int EQ, int FLUX, int RECON, bool FIN>
+__global__ void __launch_bounds__(kR3iNT * kR3iNTY, FVB_RING3_MINB)
+ring3i_kernel(const StageParams p) {
+  constexpr int DIM = 3, NT = kR3iNT, NTY = kR3iNTY, WY = kR3iRows, W = kR3iW;
+  constexpr int NC = NComp<EQ, DIM>::value;
+  constexpr int PL = WY * W;
+  constexpr int FR = NC * (NTY + 1) * NT;    // face / flux buffers: rows 0..NTY
+  extern __shared__ double smem[];
+  double* ring = smem;                          // [slot][NC][WY][W]: ring row i <-> y0-2+i, col j <-> x0-2+j
+  double* hf = ring + kRing3Slots * NC * PL;    // [NC][NTY+1][NT]: high y face of cell row i-1 (i = 0..NTY)
+  double* gf = hf + FR;                         // [NC][NTY+1][NT]: y flux below cell row i (interface (i-1|i))
+  double* hs = gf + FR;                         // [NC][NTY][NT] z recurrence: high face of the previous plane
+  double* gs = hs + NC * NTY * NT;              //                             z flux below the previous plane
+  int* rtab = reinterpret_cast<int*>(gs + NC * NTY * NT);
+  auto RG = [&](int slot, int c, int y, int x) -> double& { return ring[((slot * NC + c) * WY + y) * W + x]; };
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  auto FI = [&](int c, int y, int x) { return (c * (NTY + 1) + y) * NT + x; };
+  auto ZI = [&](int c, int y, int x) { return (c * NTY + y) * NT + x; };
+
+  const int inst = blockIdx.z / p.chunks;
+  const int chunk = blockIdx.z % p.chunks;
+  FvbState* st = p.st + (p.shared_state ? 0 : inst);
+  if (*(volatile int*)&st->done) return;
+  const double dt = p.kind == 0 ? 0.0 : *(volatile double*)&st->dt;
+  const double* __restrict__ us = p.us + p.origin + inst * p.si;
+  const double* un = p.un + p.origin + inst * p.si;
+  double* out = p.out + p.origin + inst * p.si;
+  const int64_t x0 = (int64_t)blockIdx.x * (NT - 2);
+  const int64_t y0 = (int64_t)blockIdx.y * NTY;
+  const int64_t xf = x0 - 1 + tx, yf = y0 + ty;
+  const bool cell = tx >= 1 && tx <= NT - 2 && xf < p.n[0] && yf < p.n[1];
+  const int64_t ra = p.row_lo + (int64_t)chunk * p.H;
+  const int64_t rb = min(ra + (int64_t)p.H, p.row_hi);
+  const int64_t mxf = map_index(xf, p.n[0], p.bc[0], p.g);
+  const int64_t co = mxf + map_index(yf, p.n[1], p.bc[1], p.g) * p.sy;
+  // extra copies: lanes 0 / NT-1 the x-halo columns of their row; warps 0, 1 /
+  // NTY-2, NTY-1 one y-halo row each (ring rows 0, 1 / WY-2, WY-1), interior columns
+  const bool hx_t = tx == 0 || tx == NT - 1;
+  const int64_t hxo = map_index(tx == 0 ? x0 - 2 : x0 + NT - 1, p.n[0], p.bc[0], p.g) +
+                      map_index(yf, p.n[1], p.bc[1], p.g) * p.sy;
+  const int hxc = tx == 0 ? 0 : W - 1;
+  const bool hy_t = ty <= 1 || ty >= NTY - 2;
+  const int hyr = ty <= 1 ? ty : WY - NTY + ty;  // ring row 0, 1 | WY-2, WY-1
+  const int64_t hyo = mxf + map_index(y0 - 2 + hyr, p.n[1], p.bc[1], p.g) * p.sy;
+  const int tid = ty * NT + tx;
+  for (int i = tid; i < p.H + 4; i += NT * NTY) rtab[i] = (int)(map_index(ra - 2 + i, p.n[2], p.bc[2], p.g) * p.sz);
+  __syncthreads();
+  auto roff = [&](int64_t r) -> int64_t { return rtab[r - (ra - 2)]; };
+  auto fetch = [&](int64_t r, int slot) {
+    const int64_t ro = roff(r);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, ty + 2, tx + 1), us + co + ro + c * p.sc);
+    if (hx_t) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, ty + 2, hxc), us + hxo + ro + c * p.sc);
+    }
+    if (hy_t) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, hyr, tx + 1), us + hyo + ro + c * p.sc);
+    }
+  };
+
+  unsigned errb = 0;
+  double smax[DIM] = {0.0, 0.0, 0.0};
+  double R[NC], unc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) R[c] = unc[c] = 0.0;
+
+  for (int k = 0; k < 3; ++k) {
+    fetch(ra - 2 + k, k);
+    cp_async_commit();
+  }
+  int sA = 0;
+  for (int64_t r = ra - 1; r <= rb; ++r) {
+    const int sB = (sA + 1) & 3, sC = (sA + 2) & 3;
+    if (r == ra) __syncthreads();  // iteration ra-1 had no in-plane barrier
+    if (r + 2 <= rb + 1) fetch(r + 2, (sA + 3) & 3);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();  // everybody's copies of planes <= r+1; plane r-1's y fluxes (gf) visible
+    if (r - 1 >= ra && r - 1 < rb) {  // plane r-1's y residual, deferred past this barrier
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+#if FVB_FAST
+        R[c] = fma(gf[FI(c, ty, tx)] - gf[FI(c, ty + 1, tx)], p.id[1], R[c]);
+#else
+        R[c] = R[c] - ddiv(gf[FI(c, ty + 1, tx)] - gf[FI(c, ty, tx)], p, 1);
+#endif
+      }
+    }
+    {  // z: faces of plane r, flux (r-1|r), finish plane r-1 (own column)
+      double A[NC], B[NC], C[NC], hi[NC], lo[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        A[c] = RG(sA, c, ty + 2, tx + 1);
+        B[c] = RG(sB, c, ty + 2, tx + 1);
+        C[c] = RG(sC, c, ty + 2, tx + 1);
+      }
+      weno_faces_nc<NC, RECON>(A, B, C, p.P.eps, hi, lo);
+      if (r >= ra) {
+        double H[NC], GC[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) H[c] = hs[ZI(c, ty, tx)];
+        unsigned eb = 0;
+        interface_flux<EQ, FLUX, DIM, RECON>(H, lo, A, B, 2, p.P, GC, eb);
+        if (eb && cell) errb |= 4u;
+        if (r - 1 >= ra) {
+          double v[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const double Gp = gs[ZI(c, ty, tx)];
+#if FVB_FAST
+            const double Lc = fma(Gp - GC[c], p.id[2], R[c]);
+#else
+            const double Lc = R[c] - ddiv(GC[c] - Gp, p, 2);
+#endif
+            v[c] = rk_combine(p.kind, unc[c], A[c], dt, Lc);
+          }
+          if (cell) {
+            const int64_t o = co + roff(r - 1);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
+            if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v, xf, yf, r - 1, smax);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) gs[ZI(c, ty, tx)] = GC[c];
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) hs[ZI(c, ty, tx)] = hi[c];
+    }
+    if (r >= ra && r < rb) {
+      if (p.kind >= 2 && cell) {  // u^n of plane r for the next iteration's finish
+        const int64_t o = co + roff(r);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) unc[c] = un[o + c * p.sc];
+      }
+      double B[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) B[c] = RG(sB, c, ty + 2, tx + 1);
+      if constexpr (EQ == EQ_EULER) {  // stage-start interior check (solver.py:90-93)
+        if (p.check_input && cell && !euler_physical<DIM>(B, p.P))
+          atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | flat_cell<DIM>(p, xf, yf, r));
+      }
+      // ---- x sweep: a warp is one face row; faces and fluxes by shuffle ----
+      {
+        double uL[NC], uR[NC], G[NC];
+        if constexpr (RECON != RECON_NONE) {
+          double um[NC], up[NC], hi[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            um[c] = RG(sB, c, ty + 2, tx);
+            up[c] = RG(sB, c, ty + 2, tx + 2);
+          }
+          weno_faces_nc<NC, RECON>(um, B, up, p.P.eps, hi, uR);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) uL[c] = __shfl_up_sync(0xffffffffu, hi[c], 1);
+        } else {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            uL[c] = RG(sB, c, ty + 2, tx);
+            uR[c] = B[c];
+          }
+        }
+        auto cells = [&](double* a, double* b) {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            a[c] = RG(sB, c, ty + 2, tx);
+            b[c] = RG(sB, c, ty + 2, tx + 1);
+          }
+        };
+        unsigned eb = 0;
+        interface_flux_lazy<EQ, FLUX, DIM, RECON>(uL, uR, cells, 0, p.P, G, eb);
+        if (eb && tx >= 1 && xf <= p.n[0] && yf < p.n[1]) errb |= 1u;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const double Gr = __shfl_down_sync(0xffffffffu, G[c], 1);
+#if FVB_FAST
+          R[c] = (G[c] - Gr) * p.id[0];
+#else
+          R[c] = 0.0 - ddiv(Gr - G[c], p, 0);
+#endif
+        }
+      }
+      // ---- y sweep ----
+      double lo_own[NC], hi_own[NC], lo_top[NC];
+      if constexpr (RECON != RECON_NONE) {
+        double um[NC], up[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          um[c] = RG(sB, c, ty + 1, tx + 1);
+          up[c] = RG(sB, c, ty + 3, tx + 1);
+        }
+        weno_faces_nc<NC, RECON>(um, B, up, p.P.eps, hi_own, lo_own);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) hf[FI(c, ty + 1, tx)] = hi_own[c];
+        if (ty == 0) {  // high face of row -1 (ring rows 0, 1, 2)
+          double a[NC], b[NC], d[NC], h[NC], l[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            a[c] = RG(sB, c, 0, tx + 1);
+            b[c] = RG(sB, c, 1, tx + 1);
+            d[c] = RG(sB, c, 2, tx + 1);
+          }
+          weno_faces_nc<NC, RECON>(a, b, d, p.P.eps, h, l);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) hf[FI(c, 0, tx)] = h[c];
+        }
+        if (ty == NTY - 1) {  // low face of row NTY (ring rows WY-3, WY-2, WY-1)
+          double a[NC], b[NC], d[NC], h[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            a[c] = RG(sB, c, WY - 3, tx + 1);
+            b[c] = RG(sB, c, WY - 2, tx + 1);
+            d[c] = RG(sB, c, WY - 1, tx + 1);
+          }
+          weno_faces_nc<NC, RECON>(a, b, d, p.P.eps, h, lo_top);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          hi_own[c] = lo_own[c] = B[c];
+          lo_top[c] = RG(sB, c, WY - 2, tx + 1);
+          hf[FI(c, ty + 1, tx)] = B[c];
+          if (ty == 0) hf[FI(c, 0, tx)] = RG(sB, c, 1, tx + 1);
+        }
+      }
+      __syncthreads();  // y faces visible
+      {  // interface (ty-1 | ty): uL = high face of row ty-1, uR = own low face
+        double uL[NC], G[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) uL[c] = hf[FI(c, ty, tx)];
+        auto cells = [&](double* a, double* b) {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            a[c] = RG(sB, c, ty + 1, tx + 1);
+            b[c] = B[c];
+          }
+        };
+        double uR[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) uR[c] = lo_own[c];
+        unsigned eb = 0;
+        interface_flux_lazy<EQ, FLUX, DIM, RECON>(uL, uR, cells, 1, p.P, G, eb);
+        if (eb && tx >= 1 && tx <= NT - 2 && yf <= p.n[1] && xf < p.n[0]) errb |= 2u;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) gf[FI(c, ty, tx)] = G[c];
+      }
+      if (ty == NTY - 1) {  // interface (NTY-1 | NTY)
+        double G[NC];
+        auto cells = [&](double* a, double* b) {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            a[c] = B[c];
+            b[c] = RG(sB, c, WY - 2, tx + 1);
+          }
+        };
+        unsigned eb = 0;
+        interface_flux_lazy<EQ, FLUX, DIM, RECON>(hi_own, lo_top, cells, 1, p.P, G, eb);
+        if (eb && tx >= 1 && tx <= NT - 2 && yf + 1 <= p.n[1] && xf < p.n[0]) errb |= 2u;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) gf[FI(c, NTY, tx)] = G[c];
+      }
+      // the y residual of this plane is added after the next top barrier
+    }
+    sA = sB;
+  }
+  cp_async_wait<0>();
+  if (errb) {
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+      if (errb & (1u << a))
+        atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | ((long long)(1 + a) << 40));
+  }
+  if constexpr (FIN) block_epilogue<DIM>(p, st, inst, smax, true);
+}
+
+template <int EQ>
+constexpr int ring3i_smem_bytes() {
+  constexpr int NC = NComp<EQ, 3>::value;
+  return 8 * (kRing3Slots * NC * kR3iRows * kR3iW + 2 * NC * (kR3iNTY + 1) * kR3iNT + 2 * NC * kR3iNTY * kR3iNT);
+}
+
 // Standalone wave-speed pass: solver.py:128-136 (+ the initial is_physical
 // check of solver.py:211-212).  finalize = 1 also computes the first dt.
 template <int DIM, int EQ>
