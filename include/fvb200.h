@@ -178,6 +178,11 @@ int fvb_run_stage(fvb_ctx* ctx, int stage);
  * slabs after they land (overlapped_residual, parallel.py:288-361); pass
  * last_part = 1 on the final call of a stage */
 int fvb_run_stage_rows(fvb_ctx* ctx, int stage, int64_t row_lo, int64_t row_hi, int last_part);
+/* the same stage restricted to the cell box [lo[k], hi[k]) (x, y, z; dim
+ * entries): the overlap schedule of a decomposition split along several
+ * axes (parallel.py:288-361) -- the inner box runs while every split axis's
+ * halos are in flight, then the disjoint shell slabs. */
+int fvb_run_stage_box(fvb_ctx* ctx, int stage, const int64_t* lo, const int64_t* hi, int last_part);
 int fvb_run_export(fvb_ctx* ctx, double* d_out);
 int fvb_run_finalize(fvb_ctx* ctx, const double* d_global, int post);
 /* kernel launches issued by the last fvb_run / fvb_run_steps calls */

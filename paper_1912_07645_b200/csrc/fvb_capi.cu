@@ -227,8 +227,10 @@ static int stage_occupancy(const fvb_scheme& s, const StageParams& p) {
   return best;
 }
 
-// Grid of the stage kernel; fills chunks / H / nblocks.
-static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t row_lo = 0, int64_t row_hi = -1) {
+// Grid of the stage kernel; fills chunks / H / nblocks.  xr / yr: optional
+// in-plane cell ranges [lo, hi) (x; y in 3D) of this launch.
+static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t row_lo = 0, int64_t row_hi = -1,
+                       const int64_t* xr = nullptr, const int64_t* yr = nullptr) {
   int nt, nty;
   const char* kv = getenv("FVB_KERNEL");
   // 2D default: the cp.async ring kernel; fast-mode Euler runs the pair
@@ -245,7 +247,11 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
   if (p.variant == 3 && (s.dim != 2 || s.eq != FVB_EQ_EULER)) p.variant = 2;  // pair kernel: 2D Euler
   if (s.arith == FVB_ARITH_FAST) fvb::fast::stage_block(s.dim, s.eq, p.variant, nt, nty);
   else fvb::exact::stage_block(s.dim, s.eq, p.variant, nt, nty);
-  const int64_t strips = (p.n[0] + (nt - 2) - 1) / (nt - 2);
+  p.x_lo = xr ? xr[0] : 0;
+  p.x_hi = xr ? xr[1] : p.n[0];
+  p.y_lo = yr ? yr[0] : 0;
+  p.y_hi = yr ? yr[1] : p.n[1];
+  const int64_t strips = std::max<int64_t>(1, (p.x_hi - p.x_lo + (nt - 2) - 1) / (nt - 2));
   // batched scalar ensembles on the 2D ring kernel: two instances per block
   p.ni = 1;
   if (s.dim == 2 && p.variant == 2 && s.ncomp == 1 && ninst % 2 == 0 && !p.shared_state) {
@@ -264,7 +270,7 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
     p.row_hi = row_hi;
     const int64_t nm = std::max<int64_t>(1, row_hi - row_lo);
     int64_t ytiles = 1;
-    if (s.dim == 3) ytiles = (p.n[1] + (nty - 2) - 1) / (nty - 2);
+    if (s.dim == 3) ytiles = std::max<int64_t>(1, (p.y_hi - p.y_lo + (nty - 2) - 1) / (nty - 2));
     // resident blocks per SM (register-limited) and waves of blocks: one
     // wave keeps the march long (fewer redundant halo rows per chunk)
     int64_t per_sm = s.dim == 3 ? 2 : (p.variant == 0 ? 4 : 512 / nt);  // 16 warps/SM at 128 registers
@@ -793,6 +799,34 @@ int fvb_run_stage_rows(fvb_ctx* ctx, int stage, int64_t row_lo, int64_t row_hi, 
   }
   if (row_hi <= row_lo) return FVB_OK;
   dim3 g = stage_grid(P.s, p, P.ninst, row_lo, row_hi);
+  int r = do_stage(ctx, P.s, p, g);
+  if (r) return r;
+  if (last_part && stage == P.nstages - 1) P.steps_enqueued++;
+  return FVB_OK;
+}
+
+int fvb_run_stage_box(fvb_ctx* ctx, int stage, const int64_t* lo, const int64_t* hi, int last_part) {
+  RunPlan& P = ctx->plan;
+  if (!P.active || !P.external) return set_err(ctx, FVB_E_CONFIG, "fvb_run_stage_box needs an external-reduce run");
+  if (stage < 0 || stage >= P.nstages) return set_err(ctx, FVB_E_CONFIG, "stage %d out of range", stage);
+  if (P.s.dim < 2) return set_err(ctx, FVB_E_CONFIG, "cell boxes need a march axis (dim >= 2)");
+  StageParams p = P.stage[stage];
+  if (P.s.rk_order == 1) {
+    const int par = (int)(P.steps_enqueued & 1);
+    p.us = P.bufs[par];
+    p.un = P.bufs[par];
+    p.out = P.bufs[1 - par];
+  }
+  const int march = P.s.dim - 1;
+  for (int k = 0; k < P.s.dim; ++k)
+    if (lo[k] >= hi[k]) return FVB_OK;  // empty box
+  const int64_t xr[2] = {lo[0], hi[0]};
+  const int64_t yr[2] = {lo[1], hi[1]};
+  dim3 g = stage_grid(P.s, p, P.ninst, lo[march], hi[march], xr, P.s.dim == 3 ? yr : nullptr);
+  const bool partial_plane = lo[0] != 0 || hi[0] != P.s.cells[0] ||
+                             (P.s.dim == 3 && (lo[1] != 0 || hi[1] != P.s.cells[1]));
+  if (partial_plane && !(p.variant == 2 || p.variant == 3 || p.variant == 4))
+    return set_err(ctx, FVB_E_CONFIG, "in-plane cell ranges need the ring / pair / 3D all-interior kernels");
   int r = do_stage(ctx, P.s, p, g);
   if (r) return r;
   if (last_part && stage == P.nstages - 1) P.steps_enqueued++;

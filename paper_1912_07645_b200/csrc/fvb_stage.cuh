@@ -854,10 +854,10 @@ ring_kernel(const StageParams p) {
   const double* un = p.un + p.origin + inst * p.si;
   double* out = p.out + p.origin + inst * p.si;
   const int tx = threadIdx.x;
-  const int x0 = blockIdx.x * (NT - 2);
+  const int x0 = (int)p.x_lo + blockIdx.x * (NT - 2);
   const int xf = x0 - 1 + tx;
   const int nx = (int)p.n[0];
-  const bool cell = tx >= 1 && tx <= NT - 2 && xf < nx;
+  const bool cell = tx >= 1 && tx <= NT - 2 && xf < (int)p.x_hi;
   const int ra = (int)p.row_lo + blockIdx.y * p.H;
   const int rb = min(ra + p.H, (int)p.row_hi);
   const int co = (int)map_index(xf, nx, p.bc[0], p.g);
@@ -1245,10 +1245,11 @@ pair_kernel(const StageParams p) {
   double* out = p.out + p.origin + inst * p.si;
   const int t = threadIdx.x;
   const int nx = (int)p.n[0];
-  const int x0 = blockIdx.x * (2 * kPairNT - 2);
+  const int x0 = (int)p.x_lo + blockIdx.x * (2 * kPairNT - 2);
   const int f0 = x0 - 1 + 2 * t;                     // face cells f0, f0+1 of this lane
-  const bool cell0 = t >= 1 && f0 < nx;              // updated cells (lane 0's f0 is the halo face cell)
-  const bool cell1 = t <= kPairNT - 2 && f0 + 1 < nx;
+  const int xh = (int)p.x_hi;
+  const bool cell0 = t >= 1 && f0 < xh;              // updated cells (lane 0's f0 is the halo face cell)
+  const bool cell1 = t <= kPairNT - 2 && f0 + 1 < xh;
   const int ra = (int)p.row_lo + blockIdx.y * p.H;
   const int rb = min(ra + p.H, (int)p.row_hi);
   const int co0 = (int)map_index(f0, nx, p.bc[0], p.g), co1 = (int)map_index(f0 + 1, nx, p.bc[0], p.g);
@@ -1784,10 +1785,10 @@ ring3i_kernel(const StageParams p) {
   const double* __restrict__ us = p.us + p.origin + inst * p.si;
   const double* un = p.un + p.origin + inst * p.si;
   double* out = p.out + p.origin + inst * p.si;
-  const int64_t x0 = (int64_t)blockIdx.x * (NT - 2);
-  const int64_t y0 = (int64_t)blockIdx.y * NTY;
+  const int64_t x0 = p.x_lo + (int64_t)blockIdx.x * (NT - 2);
+  const int64_t y0 = p.y_lo + (int64_t)blockIdx.y * NTY;
   const int64_t xf = x0 - 1 + tx, yf = y0 + ty;
-  const bool cell = tx >= 1 && tx <= NT - 2 && xf < p.n[0] && yf < p.n[1];
+  const bool cell = tx >= 1 && tx <= NT - 2 && xf < p.x_hi && yf < p.y_hi;
   const int64_t ra = p.row_lo + (int64_t)chunk * p.H;
   const int64_t rb = min(ra + (int64_t)p.H, p.row_hi);
   const int64_t mxf = map_index(xf, p.n[0], p.bc[0], p.g);

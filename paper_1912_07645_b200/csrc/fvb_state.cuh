@@ -193,6 +193,8 @@ struct StageParams {
   int H;              // rows per chunk
   int64_t row_lo;     // march-axis cell range computed by this launch: [row_lo, row_hi)
   int64_t row_hi;     // (inner box / shell slabs of the overlap schedule, parallel.py:288-361)
+  int64_t x_lo, x_hi; // in-plane cell ranges of this launch (x; y in 3D): the inner box / shells of
+  int64_t y_lo, y_hi; // a split in-plane axis.  Honoured by the ring, pair and 3D all-interior kernels.
   unsigned nblocks;   // blocks per state (finalize counter)
   int shared_state;   // 1: all instances are subdomains of one run (one FvbState)
   int defer_finalize; // 1: leave maxima/flags in the state; the caller reduces them

@@ -491,9 +491,10 @@ class DecomposedRun:
             self.red_host = torch.zeros(grid.dim + 2, dtype=torch.float64, pin_memory=True) if cpu_comm else None
             self.march = grid.dim - 1
             self.g = grid.ghost_width
-            self.n_march = grid.cells[self.march] if grid.dim >= 2 else 0
-            self.ovl = overlap and grid.dim >= 2 and self.march in self.split and self.n_march > 2 * self.g
-            self.other = [a for a in self.split if a != self.march]
+            # overlap schedule: every split axis long enough for an inner box
+            self.ovl = overlap and grid.dim >= 2 and bool(self.split) and \
+                all(grid.cells[a] > 2 * self.g for a in self.split)
+            self.boxes = self._boxes() if self.ovl else None
             self.nst = 1 if cfg.rk_order == 1 else cfg.rk_order
             self.steps = 0
             self.done = False
@@ -520,6 +521,26 @@ class DecomposedRun:
                 if self.topo.neighbor(self.rank, axis, side, bool(self.periodic[axis])) is None:
                     _fill_one_side(view, axis, side)
 
+    def _boxes(self):
+        """Inner box (cells >= g from every split face) and the disjoint
+        shell slabs that complete the subdomain (parallel.py:288-322): per
+        split axis two slabs of thickness g, each spanning what is left of
+        the other axes."""
+        g, dim = self.g, self.grid.dim
+        n = list(self.grid.cells)
+        lo, hi = [0] * dim, list(n)
+        inner_lo = [g if a in self.split else 0 for a in range(dim)]
+        inner_hi = [n[a] - g if a in self.split else n[a] for a in range(dim)]
+        shells = []
+        for a in self.split:
+            for side_lo, side_hi in ((0, g), (n[a] - g, n[a])):
+                blo, bhi = list(lo), list(hi)
+                blo[a], bhi[a] = side_lo, side_hi
+                shells.append((blo, bhi))
+            lo[a], hi[a] = g, n[a] - g
+        arr = lambda v: (N.C.c_int64 * 3)(*(list(v) + [0] * (3 - dim)))  # noqa: E731
+        return (arr(inner_lo), arr(inner_hi)), [(arr(a), arr(b)) for a, b in shells]
+
     def _stage(self, st, u):
         ctx, dist, topo, rank, per, grp = self.ctx, self.dist, self.topo, self.rank, self.periodic, self.group
         pack, unpack, alloc = self.halos.movers(u)
@@ -528,16 +549,14 @@ class DecomposedRun:
             self._outflow_edges(u, self.split)
             ctx.check(ctx.lib.fvb_run_stage(ctx.h, st))
             return
-        if self.other:
-            halo_exchange_dist(topo, rank, per, pack, unpack, alloc, dist, grp, axes=self.other)
-            self._outflow_edges(u, self.other)
-        g, n = self.g, self.n_march
-        handle = start_halo_exchange(topo, rank, per, pack, alloc, dist, grp, axes=[self.march])
-        ctx.check(ctx.lib.fvb_run_stage_rows(ctx.h, st, g, n - g, 0))      # inner box
+        # every split axis's halos travel while the inner box is computed
+        handle = start_halo_exchange(topo, rank, per, pack, alloc, dist, grp, axes=self.split)
+        (ilo, ihi), shells = self.boxes
+        ctx.check(ctx.lib.fvb_run_stage_box(ctx.h, st, ilo, ihi, 0))
         finish_halo_exchange(handle, unpack)
-        self._outflow_edges(u, [self.march])
-        ctx.check(ctx.lib.fvb_run_stage_rows(ctx.h, st, 0, g, 0))          # shell slabs
-        ctx.check(ctx.lib.fvb_run_stage_rows(ctx.h, st, n - g, n, 1))
+        self._outflow_edges(u, self.split)
+        for i, (blo, bhi) in enumerate(shells):
+            ctx.check(ctx.lib.fvb_run_stage_box(ctx.h, st, blo, bhi, int(i == len(shells) - 1)))
 
     def _poll(self):
         infos, done = self.run.poll()

@@ -91,7 +91,7 @@ def main():
                     if v is not None else None
             dram = (by("dram__bytes_read.sum") or 0) + (by("dram__bytes_write.sum") or 0)
             alg, how = algorithmic(cap, name)
-            if cap == "kh3d":
+            if cap in ("kh3d", "kh3d_i"):
                 # captured launches 2-4 of the run (-s 1 -c 3): RK3 stage 2, stage 3 (FIN), next step's stage 1
                 stage = (3, 3, 2)[idx] if idx < 3 else 3
                 alg, how = 512 ** 3 * 5 * 8 * stage, (f"512^3 cells x 5 comps x 8 B x {stage} (RK3 stage "
