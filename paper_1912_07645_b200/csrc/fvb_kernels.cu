@@ -117,17 +117,26 @@ static int launch_pair(const StageParams& p, dim3 grid, cudaStream_t s) {
   return launch_pdl(pair_kernel<EQ, FLUX, RECON, KS, FIN>, grid, dim3(kPairNT), smem, s, p);
 }
 
+template <int EQ, int FLUX, int RECON, int KS, bool FIN>
+static int launch_ring3i(const StageParams& p, dim3 grid, cudaStream_t s) {
+  const int smem = ring3i_smem_bytes<EQ>() + 4 * (p.H + 4);  // + plane-offset table
+  auto kern = ring3i_kernel<EQ, FLUX, RECON, KS, FIN>;
+  static unsigned done = 0;  // per instantiation
+  ensure_smem(kern, 227 * 1024, done);
+  if (grid.x == 0) return occupancy(kern, dim3(kR3iNT, kR3iNTY), smem);
+  kern<<<grid, dim3(kR3iNT, kR3iNTY), smem, s>>>(p);
+  return 0;
+}
+
 template <int DIM, int EQ, int FLUX, int RECON, bool FIN>
 static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
   if constexpr (DIM == 3) {
     if (p.variant == 4) {  // all-interior rows (default 3D)
-      const int smem = ring3i_smem_bytes<EQ>() + 4 * (p.H + 4);  // + plane-offset table
-      auto kern = ring3i_kernel<EQ, FLUX, RECON, FIN>;
-      static unsigned done = 0;  // per instantiation
-      ensure_smem(kern, 227 * 1024, done);
-      if (grid.x == 0) return occupancy(kern, dim3(kR3iNT, kR3iNTY), smem);
-      kern<<<grid, dim3(kR3iNT, kR3iNTY), smem, s>>>(p);
-      return 0;
+      const int ks = p.kind == 0 ? 0 : (p.kind == 1 ? 1 : 2);
+      if (FIN && ks == 0) return -1;
+      if (ks == 0) return launch_ring3i<EQ, FLUX, RECON, (FIN ? 1 : 0), FIN>(p, grid, s);
+      if (ks == 1) return launch_ring3i<EQ, FLUX, RECON, 1, FIN>(p, grid, s);
+      return launch_ring3i<EQ, FLUX, RECON, 2, FIN>(p, grid, s);
     }
     if (p.variant == 2) {
       const int smem = ring3_smem_bytes<EQ>() + 8 * (p.H + 4);  // + plane-offset table

@@ -1758,13 +1758,15 @@ constexpr int ring3_smem_bytes() {
 // ---------------------------------------------------------------------------
 constexpr int kR3iNT = 32, kR3iNTY = 8, kR3iRows = kR3iNTY + 4, kR3iW = kR3iNT + 2;
 
-template <int EQ, int FLUX, int RECON, bool FIN>
+
+template <int EQ, int FLUX, int RECON, int KS, bool FIN>
 __global__ void __launch_bounds__(kR3iNT * kR3iNTY, FVB_RING3_MINB)
 ring3i_kernel(const StageParams p) {
   constexpr int DIM = 3, NT = kR3iNT, NTY = kR3iNTY, WY = kR3iRows, W = kR3iW;
   constexpr int NC = NComp<EQ, DIM>::value;
   constexpr int PL = WY * W;
   constexpr int FR = NC * (NTY + 1) * NT;    // face / flux buffers: rows 0..NTY
+  constexpr bool UN = KS == 2;                 // the stage reads u^n (compile time: no u^n registers otherwise)
   extern __shared__ double smem[];
   double* ring = smem;                          // [slot][NC][WY][W]: ring row i <-> y0-2+i, col j <-> x0-2+j
   double* hf = ring + kRing3Slots * NC * PL;    // [NC][NTY+1][NT]: high y face of cell row i-1 (i = 0..NTY)
@@ -1781,7 +1783,7 @@ ring3i_kernel(const StageParams p) {
   const int chunk = blockIdx.z % p.chunks;
   FvbState* st = p.st + (p.shared_state ? 0 : inst);
   if (*(volatile int*)&st->done) return;
-  const double dt = p.kind == 0 ? 0.0 : *(volatile double*)&st->dt;
+  const double dt = KS == 0 ? 0.0 : *(volatile double*)&st->dt;
   const double* __restrict__ us = p.us + p.origin + inst * p.si;
   const double* un = p.un + p.origin + inst * p.si;
   double* out = p.out + p.origin + inst * p.si;
@@ -1822,9 +1824,11 @@ ring3i_kernel(const StageParams p) {
 
   unsigned errb = 0;
   double smax[DIM] = {0.0, 0.0, 0.0};
-  double R[NC], unc[NC];
+  double R[NC], unc[UN ? NC : 1];
 #pragma unroll
-  for (int c = 0; c < NC; ++c) R[c] = unc[c] = 0.0;
+  for (int c = 0; c < NC; ++c) R[c] = 0.0;
+#pragma unroll
+  for (int c = 0; c < (UN ? NC : 1); ++c) unc[c] = 0.0;
 
   for (int k = 0; k < 3; ++k) {
     fetch(ra - 2 + k, k);
@@ -1874,7 +1878,7 @@ ring3i_kernel(const StageParams p) {
 #else
             const double Lc = R[c] - ddiv(GC[c] - Gp, p, 2);
 #endif
-            v[c] = rk_combine(p.kind, unc[c], A[c], dt, Lc);
+            v[c] = KS == 0 ? Lc : rk_combine(p.kind, UN ? unc[UN ? c : 0] : 0.0, A[c], dt, Lc);
           }
           if (cell) {
             const int64_t o = co + roff(r - 1);
@@ -1890,10 +1894,12 @@ ring3i_kernel(const StageParams p) {
       for (int c = 0; c < NC; ++c) hs[ZI(c, ty, tx)] = hi[c];
     }
     if (r >= ra && r < rb) {
-      if (p.kind >= 2 && cell) {  // u^n of plane r for the next iteration's finish
-        const int64_t o = co + roff(r);
+      if constexpr (UN) {
+        if (cell) {  // u^n of plane r for the next iteration's finish
+          const int64_t o = co + roff(r);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) unc[c] = un[o + c * p.sc];
+          for (int c = 0; c < NC; ++c) unc[c] = un[o + c * p.sc];
+        }
       }
       double B[NC];
 #pragma unroll
