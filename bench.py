@@ -501,6 +501,7 @@ def bench_kh3d(args, env):
     run.advance(1)
     final, _ = run.finish()
     cells = n ** 3
+    field_bytes = 5 * (n + 4) ** 3 * 8
     ms_per_step = t_ms / args.steps
     value = ws * cells * 3 * args.steps / (t_ms * 1e-3) / 1e9
     roof = _roofline(8 * 5 * 8 / 3, ws * cells * 3 * args.steps, t_ms * 1e-3,
@@ -510,20 +511,25 @@ def bench_kh3d(args, env):
     roof["per"] = "GPU"
 
     # e2e: this rank's subdomain from pinned host memory through DecomposedRun
-    # (H2D inside), e2e_steps RK3 steps, final subdomain back to the host
-    host = pinned_field(final.to_host())
-    m = max(1, args.e2e_steps // 2)
-    env.barrier()
-    tic = time.perf_counter()
-    r2 = DecomposedRun(host, cfg, topo, n_steps=m, arith=args.arith, log=False)
-    r2.advance()
-    out, _ = r2.finish()
-    out.to_host()
-    torch.cuda.synchronize()
-    el = env.max_over_ranks(time.perf_counter() - tic)
-    e2e = {"value": round(ws * cells * 3 * m / el / 1e9, 4), "unit": UNIT,
-           "h2d_bytes_per_step": int(host.data.nbytes), "d2h_bytes_per_step": int(host.data.nbytes),
-           "step": f"one DecomposedRun of {m} RK3 steps per rank from a pinned host subdomain, result to host"}
+    # (H2D inside), e2e_steps RK3 steps, final subdomain back to the host --
+    # for subdomains up to 8 GB (a 1024^3 subdomain would need 43 GB of
+    # pinned host memory per rank and a second set of device buffers)
+    e2e = None
+    if field_bytes <= 8 << 30:
+        host = pinned_field(final.to_host())
+        del final, run
+        m = max(1, args.e2e_steps // 2)
+        env.barrier()
+        tic = time.perf_counter()
+        r2 = DecomposedRun(host, cfg, topo, n_steps=m, arith=args.arith, log=False)
+        r2.advance()
+        out, _ = r2.finish()
+        out.to_host()
+        torch.cuda.synchronize()
+        el = env.max_over_ranks(time.perf_counter() - tic)
+        e2e = {"value": round(ws * cells * 3 * m / el / 1e9, 4), "unit": UNIT,
+               "h2d_bytes_per_step": int(host.data.nbytes), "d2h_bytes_per_step": int(host.data.nbytes),
+               "step": f"one DecomposedRun of {m} RK3 steps per rank from a pinned host subdomain, result to host"}
     return {"value": value, "ms_per_step": ms_per_step, "roofline": roof, "e2e": e2e, "launches": launches,
             "clocks": clk.summary(), "t_start": 0.0, "stats": None,
             "state": f"KH3D from t = 0 after {args.warmup} warm-up steps",

@@ -154,6 +154,8 @@ static int validate(fvb_ctx* ctx, const fvb_scheme* s) {
 static int validate_instances(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, int ninst, bool scratch) {
   if (ninst < 1) return set_err(ctx, FVB_E_CONFIG, "ninst must be >= 1");
   if (scratch && ninst > 4096) return set_err(ctx, FVB_E_CONFIG, "too many instances (%d > 4096)", ninst);
+  if (lay && s->dim == 3 && (s->cells[0] + 2 * s->ghost) * (s->cells[1] + 2 * s->ghost) * (s->cells[2] + 2 * s->ghost) >= (int64_t(1) << 31))
+    return set_err(ctx, FVB_E_CONFIG, "3D instance component exceeds the 32-bit kernel offsets (2^31 cells)");
   if (lay && s->dim == 2) {
     const int64_t g = s->ghost;
     const int64_t span = (int64_t)(s->ncomp - 1) * lay->sc + (s->cells[1] + 2 * g) * lay->sy + s->cells[0] + 2 * g;
@@ -230,7 +232,7 @@ static int stage_occupancy(const fvb_scheme& s, const StageParams& p) {
 // Grid of the stage kernel; fills chunks / H / nblocks.  xr / yr: optional
 // in-plane cell ranges [lo, hi) (x; y in 3D) of this launch.
 static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t row_lo = 0, int64_t row_hi = -1,
-                       const int64_t* xr = nullptr, const int64_t* yr = nullptr) {
+                       const int64_t* xr = nullptr, const int64_t* yr = nullptr, int force_variant = -1) {
   int nt, nty;
   const char* kv = getenv("FVB_KERNEL");
   // 2D default: the cp.async ring kernel; fast-mode Euler runs the pair
@@ -238,13 +240,17 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
   // FVB_KERNEL=ring / pair / tile / strip select explicitly.
   p.variant = (s.dim == 2 && s.eq == FVB_EQ_EULER && s.arith == FVB_ARITH_FAST) ? 3 : 2;
   if (kv && std::strcmp(kv, "ring") == 0) p.variant = 2;
-  if (s.dim == 3 && p.variant == 2) p.variant = 4;  // 3D default: all-interior-rows ring kernel
+  // 3D default: the all-interior-rows ring kernel in fast mode; exact mode
+  // keeps the round-1 ring3 kernel (measured faster with the IEEE sequences)
+  if (s.dim == 3 && p.variant == 2 && s.arith == FVB_ARITH_FAST) p.variant = 4;
+  if (kv && std::strcmp(kv, "ring3i") == 0 && s.dim == 3) p.variant = 4;
   if (kv && std::strcmp(kv, "ring3") == 0) p.variant = 2;
   if (kv && std::strcmp(kv, "strip") == 0) p.variant = 0;
   if (kv && std::strcmp(kv, "tile") == 0) p.variant = 1;
   if (kv && std::strcmp(kv, "pair") == 0) p.variant = 3;
   if (s.dim == 1 && p.variant >= 2) p.variant = 1;
   if (p.variant == 3 && (s.dim != 2 || s.eq != FVB_EQ_EULER)) p.variant = 2;  // pair kernel: 2D Euler
+  if (force_variant >= 0) p.variant = force_variant;
   if (s.arith == FVB_ARITH_FAST) fvb::fast::stage_block(s.dim, s.eq, p.variant, nt, nty);
   else fvb::exact::stage_block(s.dim, s.eq, p.variant, nt, nty);
   p.x_lo = xr ? xr[0] : 0;
@@ -825,7 +831,12 @@ int fvb_run_stage_box(fvb_ctx* ctx, int stage, const int64_t* lo, const int64_t*
   dim3 g = stage_grid(P.s, p, P.ninst, lo[march], hi[march], xr, P.s.dim == 3 ? yr : nullptr);
   const bool partial_plane = lo[0] != 0 || hi[0] != P.s.cells[0] ||
                              (P.s.dim == 3 && (lo[1] != 0 || hi[1] != P.s.cells[1]));
-  if (partial_plane && !(p.variant == 2 || p.variant == 3 || p.variant == 4))
+  if (partial_plane && P.s.dim == 3 && p.variant == 2)
+    // in-plane ranges: the 3D all-interior kernel (same arithmetic, bitwise
+    // equal to ring3 in both modes) instead of ring3, which has none
+    g = stage_grid(P.s, p, P.ninst, lo[march], hi[march], xr, yr, 4);
+  const bool ranged = P.s.dim == 2 ? (p.variant == 2 || p.variant == 3) : p.variant == 4;
+  if (partial_plane && !ranged)
     return set_err(ctx, FVB_E_CONFIG, "in-plane cell ranges need the ring / pair / 3D all-interior kernels");
   int r = do_stage(ctx, P.s, p, g);
   if (r) return r;

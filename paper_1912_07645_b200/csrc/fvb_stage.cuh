@@ -9,14 +9,24 @@
 //
 // Work decomposition (B200):
 //  * The slowest axis (y in 2D, z in 3D) is MARCHED: a block owns a strip of
-//    NT (x) [x NTY (y, 3D)] columns and walks H rows along the march axis.
-//    Each thread keeps a 3-row register window of its column, so the
+//    columns (x [, y]) and walks H rows (planes) of one march chunk, so the
 //    march-axis faces and fluxes are computed exactly once per cell and each
 //    cell of u^s is read from HBM once per stage.
-//  * The in-plane axes (x; x and y in 3D) go through shared memory one row
-//    at a time.  Thread <-> "face cell" mapping: NT threads cover NT-2
-//    updated cells plus one halo face cell each side, so every WENO face pair
-//    is computed once per row and each interface flux once (+2/NT halo).
+//  * Kernels, by default use:
+//      pair_kernel   2D Euler, fast mode: one-warp blocks, two x-columns per
+//                    lane, rows in a cp.async shared-memory ring (16-byte
+//                    copies), x neighbours by shuffle.
+//      ring_kernel   2D otherwise: one column per thread, the same ring.
+//      ring3i_kernel 3D: 32 x 8 threads own a 30 x 8 cell tile, planes in a
+//                    cp.async ring, x sweep by shuffle, y sweep via shared
+//                    memory, every warp an interior row.
+//      stage_kernel  1D (and the FVB_KERNEL=tile alternative in 2D / 3D):
+//                    per-thread register window.
+//    Alternatives for A/B runs: strip_kernel (FVB_KERNEL=strip), ring3_kernel
+//    (FVB_KERNEL=ring3, the round-1 3D kernel).
+//  * Thread <-> "face cell" mapping: a block's threads cover its updated
+//    cells plus one halo face cell each side in x, so every WENO face pair is
+//    computed once per row and each interface flux once (+2 per strip).
 //  * Ghost cells are never materialised for periodic/outflow axes: indices
 //    outside the interior are wrapped/clamped on load, which reproduces
 //    fill_boundary (grid.py:147-175) exactly; FVB_BC_HALO axes read ghosts
@@ -528,7 +538,7 @@ constexpr int stage_smem_bytes() {
 }
 
 // ---------------------------------------------------------------------------
-// Warp-strip kernel (1D and 2D): the production path for the 2D configs.
+// Warp-strip kernel (1D and 2D; FVB_KERNEL=strip, an A/B alternative).
 //
 // Each WARP owns a strip of 30 cells in x (lanes 1..30; lanes 0 and 31 are
 // the halo face cells) and marches along y over one chunk of rows.  x

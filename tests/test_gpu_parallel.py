@@ -108,3 +108,23 @@ def test_protocol_errors(P):
         tr.send(PP.HaloMessage(0, 1, 0, 1, 5, np.zeros(1)))
     with pytest.raises(P.ProtocolError):
         tr.receive(0, 1, 1, 1, 5)
+
+
+@pytest.mark.parametrize("name,layouts", [("kh2d64_weno2_50", [(2, 1), (1, 2), (2, 2)]),
+                                          ("euler2d_hllc_weno3_outflow", [(2, 1), (2, 2)]),
+                                          ("kh3d16_weno2_5", [(2, 2, 2), (1, 2, 1)])])
+def test_run_parallel_fast_decomposition_invariant(P, golden, golden_arrays, name, layouts):
+    """Fast mode (the pair kernel in 2D, ring3i in 3D, ghosts of split axes
+    read from memory incl. the 16-byte ring copies): a decomposed run equals
+    the undecomposed fast run bitwise -- the reference's decomposition
+    invariance (tests/test_parallel.py:192-212) holds in both modes."""
+    from paper_1912_07645_b200.parallel import run_parallel
+
+    case = next(r for r in golden["runs"] if r["name"] == name)
+    grid, cfg = product_objects(case["scheme"])
+    data = np.array(golden_arrays[name + "__init"])
+    init = P.Field(grid, data.shape[0], data)
+    whole, _ = run_parallel(init, cfg, (1,) * grid.dim, n_steps=5, arith="fast")
+    for lay in layouts:
+        out, recs = run_parallel(init, cfg, lay, n_steps=5, arith="fast")
+        assert O.sha16(out.interior) == O.sha16(whole.interior), (name, lay)

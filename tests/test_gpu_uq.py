@@ -185,3 +185,21 @@ def test_run_mlmc_with_device_init(P, golden):
     if O.sha16(res.mean) != case["mean_sha"]:
         assert rel_l1(res.mean, ref.mean) <= 1e-12
     assert rel_l1(res.variance, ref.variance) <= 1e-10
+
+
+@pytest.mark.parametrize("H,p", [(70, 2.0), (9, 1.0), (12, 1.5)])
+def test_structure_function_any_max_offset(P, H, p):
+    """StructureFunctionAccumulator.update (uq.py:254-262) with max offsets
+    past the old 63 limit, offsets longer than the grid (np.roll wraps) and
+    p != 2, against the oracle's numpy restatement."""
+    from paper_1912_07645_b200 import uq
+
+    rng = np.random.default_rng(H)
+    grid = P.GridSpec(2, (48, 40), (0.0, 0.0), (1.0, 1.0), ghost_width=2)
+    data = np.zeros((1, 44, 52))
+    data[0, 2:42, 2:50] = rng.standard_normal((40, 48))
+    sf = uq.StructureFunctionAccumulator(p, H)
+    sf.update(P.Field(grid, 1, data))
+    ref = O.structure_sums(data[0, 2:42, 2:50], p, H)
+    assert sf.samples == 1 and len(sf.sums) == H + 1
+    assert rel_l1(sf.sums, ref) <= 1e-13
