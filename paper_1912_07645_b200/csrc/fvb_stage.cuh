@@ -1222,9 +1222,6 @@ __device__ __forceinline__ void cp_async16(double* dst, const double* src) {
 constexpr int kPairNT = 32;                // one warp
 constexpr int kPairW = 2 * kPairNT + 2;    // ring row width: cells x0-2 .. x0+63
 
-#ifndef FVB_PAIR_LAZY
-#define FVB_PAIR_LAZY 1  // fallback cells / u^s of the finished row re-read from the ring instead of held in registers
-#endif
 #ifndef FVB_PAIR_MINB
 #define FVB_PAIR_MINB 12  // <= 168 registers: 12 one-warp blocks/SM (measured: 23.5 vs 22.9 at 8, 17.8 at 14 -- spills)
 #endif
@@ -1379,7 +1376,6 @@ pair_kernel(const StageParams p) {
           H1[c] = h.y;
         }
         unsigned eb0 = 0, eb1 = 0;
-#if FVB_PAIR_LAZY
         // fallback cells reloaded from the ring only when needed: no stencil
         // registers held live across the flux
         interface_flux_lazy<EQ, FLUX, DIM, RECON>(H0, lo0, [&](double* a, double* b) {
@@ -1390,10 +1386,6 @@ pair_kernel(const StageParams p) {
 #pragma unroll
           for (int c = 0; c < NC; ++c) { a[c] = RG(sA, c, 2 * t + 2); b[c] = RG(sB, c, 2 * t + 2); }
         }, 1, p.P, G1, eb1);
-#else
-        interface_flux<EQ, FLUX, DIM, RECON>(H0, lo0, A0, P1, 1, p.P, G0, eb0);
-        interface_flux<EQ, FLUX, DIM, RECON>(H1, lo1, A1, P2, 1, p.P, G1, eb1);
-#endif
         if ((eb0 && cell0) || (eb1 && cell1)) errb |= 2u;
         if (r - 1 >= ra) {
           double v0[NC], v1[NC];
@@ -1408,11 +1400,7 @@ pair_kernel(const StageParams p) {
               un1 = u2.y;
             }
 #if FVB_FAST
-#if FVB_PAIR_LAZY
             const double a0c = RG(sA, c, 2 * t + 1), a1c = RG(sA, c, 2 * t + 2);  // u^s of row r-1, re-read
-#else
-            const double a0c = A0[c], a1c = A1[c];
-#endif
             double b0 = KS == 0 ? 0.0 : (KS == 1 ? a0c : fma(rk_b, a0c, rk_a * un0));
             double b1 = KS == 0 ? 0.0 : (KS == 1 ? a1c : fma(rk_b, a1c, rk_a * un1));
             v0[c] = fma(cy, gp.x - G0[c], fma(cxs, xr.x, b0));
@@ -1460,7 +1448,6 @@ pair_kernel(const StageParams p) {
       for (int c = 0; c < NC; ++c) uLa[c] = __shfl_up_sync(0xffffffffu, hi1[c], 1);  // f0-1's high face
       unsigned eba = 0, ebb = 0;
       // interface (f0-1 | f0): cells P0, P1; interface (f0 | f1): cells P1, P2 (fallback operands)
-#if FVB_PAIR_LAZY
       interface_flux_lazy<EQ, FLUX, DIM, RECON>(uLa, lo0, [&](double* a, double* b) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) { a[c] = RG(sB, c, 2 * t); b[c] = RG(sB, c, 2 * t + 1); }
@@ -1469,10 +1456,6 @@ pair_kernel(const StageParams p) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) { a[c] = RG(sB, c, 2 * t + 1); b[c] = RG(sB, c, 2 * t + 2); }
       }, 0, p.P, Gb, ebb);
-#else
-      interface_flux<EQ, FLUX, DIM, RECON>(uLa, lo0, P0, P1, 0, p.P, Ga, eba);
-      interface_flux<EQ, FLUX, DIM, RECON>(hi0, lo1, P1, P2, 0, p.P, Gb, ebb);
-#endif
       if ((eba && t >= 1 && f0 <= nx) || (ebb && f0 + 1 <= nx)) errb |= 1u;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
