@@ -188,3 +188,17 @@ def test_c5_burgers_qmc_2048_4_samples(P, jobs, pool, arith):
         assert rel_l1(m.acc.variance(ddof=1), ref.variance()) <= 1e-10
         assert rel_l1(s.sums, sf) <= 1e-12
     assert s.samples == 4
+
+
+def test_kh3d_128_fast_one_step(P, jobs):
+    """The fast-mode 3D default (ring3i) at 128^3 against the oracle.  At t = 0
+    the y/z momenta are pure pressure round-off (vy = vz = 0), so their error
+    is measured against 1e-3 of the largest component's norm (helpers.rel_l1_field)."""
+    from paper_1912_07645_b200.initial import kelvin_helmholtz
+    from tests.helpers import rel_l1_field
+
+    grid, cfg = _kh_objects(P, 128, dim=3)
+    out, recs = P.run_simulation(kelvin_helmholtz(grid, KH_VEC), cfg, max_steps=1, arith="fast")
+    ref, dts = jobs["kh3d"].result()[1]
+    assert rel_l1_field(out.interior, ref) <= 1e-12
+    assert abs(recs[0].dt - dts[0]) <= 1e-12 * dts[0]

@@ -211,12 +211,14 @@ def test_fast_mode_divergence_growth(P, golden, golden_arrays, name):
     ("tile", "euler3d_tiles_hllc_weno2"), ("tile", "burgers3d_weno3_rk2_outflow"), ("tile", "kh3d16_weno2_5"),
     ("pair", "kh2d64_weno2_50"), ("pair", "euler2d_hllc_weno3_outflow"), ("pair", "euler2d_rusanov_weno2_outflow"),
     ("ring3", "euler3d_tiles_hllc_weno2"), ("ring3", "kh3d16_weno2_5"),
+    ("ring3i", "euler3d_tiles_hllc_weno2"), ("ring3i", "kh3d16_weno2_5"), ("ring3i", "burgers3d_weno3_rk2_outflow"),
+    ("ring3i", "euler3d_hllc_none_outflow"),
 ])
 def test_alternate_stage_kernels_bitwise(P, golden, golden_arrays, monkeypatch, kernel, name):
     """The non-default stage kernels (FVB_KERNEL=tile / strip: register-window
     tile and warp-strip variants; pair: the fast-mode 2D Euler default, here
-    in exact arithmetic; ring3: the round-1 3D kernel) reproduce the
-    reference bitwise too."""
+    in exact arithmetic; ring3 / ring3i: the two 3D ring kernels, ring3i
+    being the fast-mode default) reproduce the reference bitwise too."""
     monkeypatch.setenv("FVB_KERNEL", kernel)
     case = next(r for r in golden["runs"] if r["name"] == name)
     grid, cfg = product_objects(case["scheme"])
