@@ -249,7 +249,7 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
   if (kv && std::strcmp(kv, "tile") == 0) p.variant = 1;
   if (kv && std::strcmp(kv, "pair") == 0) p.variant = 3;
   if (s.dim == 1 && p.variant >= 2) p.variant = 1;
-  if (p.variant == 3 && (s.dim != 2 || s.eq != FVB_EQ_EULER)) p.variant = 2;  // pair kernel: 2D Euler
+  if (p.variant == 3 && s.dim != 2) p.variant = 2;  // pair kernel: 2D (default for fast-mode Euler)
   if (force_variant >= 0) p.variant = force_variant;
   if (s.arith == FVB_ARITH_FAST) fvb::fast::stage_block(s.dim, s.eq, p.variant, nt, nty);
   else fvb::exact::stage_block(s.dim, s.eq, p.variant, nt, nty);

@@ -148,8 +148,8 @@ static int launch_fin(const StageParams& p, dim3 grid, cudaStream_t s) {
       return 0;
     }
   }
-  if constexpr (DIM == 2 && EQ == EQ_EULER) {
-    if (p.variant == 3) {  // two x-columns per thread (Euler)
+  if constexpr (DIM == 2) {
+    if (p.variant == 3) {  // two x-columns per thread
       const int ks = p.kind == 0 ? 0 : (p.kind == 1 ? 1 : 2);
       if (FIN && ks == 0) return -1;
       if (ks == 0) return launch_pair<EQ, FLUX, RECON, (FIN ? 1 : 0), FIN>(p, grid, s);

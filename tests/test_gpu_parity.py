@@ -210,6 +210,7 @@ def test_fast_mode_divergence_growth(P, golden, golden_arrays, name):
     ("strip", "kh2d64_weno2_50"), ("strip", "euler2d_rusanov_weno2_outflow"), ("strip", "burgers1d_weno3_rk3_outflow"),
     ("tile", "euler3d_tiles_hllc_weno2"), ("tile", "burgers3d_weno3_rk2_outflow"), ("tile", "kh3d16_weno2_5"),
     ("pair", "kh2d64_weno2_50"), ("pair", "euler2d_hllc_weno3_outflow"), ("pair", "euler2d_rusanov_weno2_outflow"),
+    ("pair", "burgers2d64_qmc0"), ("pair", "advection2d_weno3_rk3"), ("pair", "advection2d_none_rk2"),
     ("ring3", "euler3d_tiles_hllc_weno2"), ("ring3", "kh3d16_weno2_5"),
     ("ring3i", "euler3d_tiles_hllc_weno2"), ("ring3i", "kh3d16_weno2_5"), ("ring3i", "burgers3d_weno3_rk2_outflow"),
     ("ring3i", "euler3d_hllc_none_outflow"),
