@@ -235,10 +235,10 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
                        const int64_t* xr = nullptr, const int64_t* yr = nullptr, int force_variant = -1) {
   int nt, nty;
   const char* kv = getenv("FVB_KERNEL");
-  // 2D default: the cp.async ring kernel; fast-mode Euler runs the pair
-  // kernel (two x-columns per thread).
+  // 2D default: the pair kernel (two x-columns per thread, DESIGN.md
+  // section 3) in fast mode, the cp.async ring kernel in exact mode.
   // FVB_KERNEL=ring / pair / tile / strip select explicitly.
-  p.variant = (s.dim == 2 && s.eq == FVB_EQ_EULER && s.arith == FVB_ARITH_FAST) ? 3 : 2;
+  p.variant = (s.dim == 2 && s.arith == FVB_ARITH_FAST) ? 3 : 2;
   if (kv && std::strcmp(kv, "ring") == 0) p.variant = 2;
   // 3D default: the all-interior-rows ring kernel in fast mode; exact mode
   // keeps the round-1 ring3 kernel (measured faster with the IEEE sequences)
@@ -249,7 +249,7 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
   if (kv && std::strcmp(kv, "tile") == 0) p.variant = 1;
   if (kv && std::strcmp(kv, "pair") == 0) p.variant = 3;
   if (s.dim == 1 && p.variant >= 2) p.variant = 1;
-  if (p.variant == 3 && s.dim != 2) p.variant = 2;  // pair kernel: 2D (default for fast-mode Euler)
+  if (p.variant == 3 && s.dim != 2) p.variant = 2;  // pair kernel: 2D only
   if (force_variant >= 0) p.variant = force_variant;
   if (s.arith == FVB_ARITH_FAST) fvb::fast::stage_block(s.dim, s.eq, p.variant, nt, nty);
   else fvb::exact::stage_block(s.dim, s.eq, p.variant, nt, nty);
