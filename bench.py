@@ -350,7 +350,8 @@ def bench_single(args, env):
     ms_per_step = t_ms / args.steps
     value = env.ws * cells * 3 * args.steps / (t_ms * 1e-3) / 1e9
     bps = 8 * ncomp * (2 + 3 + 3) / 3  # stage 1: r us, w out; stages 2-3: r us, un, w out
-    kname = ("ring_kernel<BURGERS,RUSANOV,WENO2> (batched)" if burgers else "ring_kernel<EULER,HLLC,WENO2>")
+    kern = "pair_kernel" if args.arith == "fast" else "ring_kernel"  # fvb_capi.cu stage_grid defaults
+    kname = (f"{kern}<BURGERS,RUSANOV,WENO2> (batched)" if burgers else f"{kern}<EULER,HLLC,WENO2>")
     roof = _roofline(bps, cells * 3 * args.steps, t_ms * 1e-3, kname + " (3 launches/step)")
     if not burgers:
         _kh2d_profile_keys(roof)
@@ -435,7 +436,8 @@ def bench_mc(args, env):
     assert result["m"].acc.count == M
     bps = 85.33 + 160.0 / (3 * S)  # + the per-sample moments update (read field, rmw mean and M2)
     roof = _roofline(bps, cell_stages * args.steps, t_ms * 1e-3,
-                     "ring_kernel<EULER,HLLC,WENO2> (batched) + moments_push_kernel")
+                     ("pair_kernel" if args.arith == "fast" else "ring_kernel")
+                     + "<EULER,HLLC,WENO2> (batched) + moments_push_kernel")
 
     # e2e: the same sharded run_mc with the caller's host evaluate_init (the
     # reference-style numpy initial data, H2D of every sample) and the
@@ -505,7 +507,8 @@ def bench_kh3d(args, env):
     ms_per_step = t_ms / args.steps
     value = ws * cells * 3 * args.steps / (t_ms * 1e-3) / 1e9
     roof = _roofline(8 * 5 * 8 / 3, ws * cells * 3 * args.steps, t_ms * 1e-3,
-                     "ring3_kernel<EULER,HLLC,WENO2> (3+ launches/step)")
+                     ("ring3i_kernel" if args.arith == "fast" else "ring3_kernel")
+                     + "<EULER,HLLC,WENO2> (3+ launches/step)")
     roof["achieved"] = round(roof["achieved"] / ws, 1)  # per GPU (the peak is one GPU's)
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
     roof["per"] = "GPU"
