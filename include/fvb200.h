@@ -183,6 +183,15 @@ int fvb_run_stage_rows(fvb_ctx* ctx, int stage, int64_t row_lo, int64_t row_hi, 
  * axes (parallel.py:288-361) -- the inner box runs while every split axis's
  * halos are in flight, then the disjoint shell slabs. */
 int fvb_run_stage_box(fvb_ctx* ctx, int stage, const int64_t* lo, const int64_t* hi, int last_part);
+/* fused halo exchange (parallel.py:201-254 without the message step): with
+ * the march axis (y in 2D, z in 3D) split, lo[k] / hi[k] are the low / high
+ * neighbour's copies of bufs[k] -- peer memory over NVLink (CUDA IPC /
+ * symmetric memory), identical layout.  Every stage then also stores its
+ * first / last g march rows into the neighbour's ghost rows of the buffer it
+ * writes; the caller orders stages across ranks (a device barrier after each
+ * stage).  lo or hi may be NULL (world edge).  External-reduce runs, one
+ * subdomain per context. */
+int fvb_run_set_peers(fvb_ctx* ctx, double* const* lo, double* const* hi);
 int fvb_run_export(fvb_ctx* ctx, double* d_out);
 int fvb_run_finalize(fvb_ctx* ctx, const double* d_global, int post);
 /* kernel launches issued by the last fvb_run / fvb_run_steps calls */

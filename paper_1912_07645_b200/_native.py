@@ -82,6 +82,7 @@ _SIGS = {
     "fvb_run_stage": ([C.c_void_p, C.c_int], C.c_int),
     "fvb_run_stage_rows": ([C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int], C.c_int),
     "fvb_run_stage_box": ([C.c_void_p, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_int], C.c_int),
+    "fvb_run_set_peers": ([C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)], C.c_int),
     "fvb_run_export": ([C.c_void_p, C.c_void_p], C.c_int),
     "fvb_run_finalize": ([C.c_void_p, C.c_void_p, C.c_int], C.c_int),
     "fvb_run_read_log": ([C.c_void_p, C.POINTER(C.c_double), C.c_int64], C.c_int),

@@ -75,6 +75,8 @@ struct RunPlan {
   int topo;          // instances are the subdomains of one decomposed run
   int ranks[3];
   int periodic[3];
+  double* peer[2][3];  // fused halo exchange: the low / high march-axis neighbour's bufs[k] (peer memory)
+  int peer_on;
 };
 
 struct fvb_ctx {
@@ -774,6 +776,36 @@ int fvb_run_set_external_reduce(fvb_ctx* ctx, int on) {
   return FVB_OK;
 }
 
+// Peer buffers of the stage's output (fused halo exchange, fvb_run_set_peers).
+static void apply_peers(const RunPlan& P, StageParams& p) {
+  p.peer_lo = p.peer_hi = nullptr;
+  if (!P.peer_on) return;
+  int k = -1;
+  for (int i = 0; i < 3; ++i)
+    if (P.bufs[i] == p.out) k = i;
+  if (k < 0) return;
+  const int march = P.s.dim - 1;
+  p.n_march = P.s.cells[march];
+  p.peer_shift = p.n_march * (P.s.dim == 2 ? P.L.sy : P.L.sz);
+  if (P.peer[0][k]) p.peer_lo = P.peer[0][k] + P.L.origin;
+  if (P.peer[1][k]) p.peer_hi = P.peer[1][k] + P.L.origin;
+}
+
+int fvb_run_set_peers(fvb_ctx* ctx, double* const* lo, double* const* hi) {
+  RunPlan& P = ctx->plan;
+  if (!P.active || !P.external) return set_err(ctx, FVB_E_CONFIG, "fvb_run_set_peers needs an external-reduce run");
+  if (P.s.dim < 2) return set_err(ctx, FVB_E_CONFIG, "fused halo exchange needs a march axis (dim >= 2)");
+  if (P.ninst != 1) return set_err(ctx, FVB_E_CONFIG, "fused halo exchange is per subdomain (ninst == 1)");
+  if (P.s.bc[P.s.dim - 1] != FVB_BC_HALO)
+    return set_err(ctx, FVB_E_CONFIG, "fused halo exchange: the march axis must be a halo (split) axis");
+  for (int k = 0; k < 3; ++k) {
+    P.peer[0][k] = lo ? lo[k] : nullptr;
+    P.peer[1][k] = hi ? hi[k] : nullptr;
+  }
+  P.peer_on = (lo != nullptr) || (hi != nullptr);
+  return FVB_OK;
+}
+
 int fvb_run_stage(fvb_ctx* ctx, int stage) {
   RunPlan& P = ctx->plan;
   if (!P.active || !P.external) return set_err(ctx, FVB_E_CONFIG, "fvb_run_stage needs an external-reduce run");
@@ -785,6 +817,7 @@ int fvb_run_stage(fvb_ctx* ctx, int stage) {
     p.un = P.bufs[par];
     p.out = P.bufs[1 - par];
   }
+  apply_peers(P, p);
   int r = do_stage(ctx, P.s, p, P.grid);
   if (r) return r;
   if (stage == P.nstages - 1) P.steps_enqueued++;
@@ -805,6 +838,7 @@ int fvb_run_stage_rows(fvb_ctx* ctx, int stage, int64_t row_lo, int64_t row_hi, 
   }
   if (row_hi <= row_lo) return FVB_OK;
   dim3 g = stage_grid(P.s, p, P.ninst, row_lo, row_hi);
+  apply_peers(P, p);
   int r = do_stage(ctx, P.s, p, g);
   if (r) return r;
   if (last_part && stage == P.nstages - 1) P.steps_enqueued++;
@@ -838,6 +872,7 @@ int fvb_run_stage_box(fvb_ctx* ctx, int stage, const int64_t* lo, const int64_t*
   const bool ranged = P.s.dim == 2 ? (p.variant == 2 || p.variant == 3) : p.variant == 4;
   if (partial_plane && !ranged)
     return set_err(ctx, FVB_E_CONFIG, "in-plane cell ranges need the ring / pair / 3D all-interior kernels");
+  apply_peers(P, p);
   int r = do_stage(ctx, P.s, p, g);
   if (r) return r;
   if (last_part && stage == P.nstages - 1) P.steps_enqueued++;

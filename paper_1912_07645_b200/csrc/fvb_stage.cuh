@@ -73,6 +73,18 @@ __device__ __forceinline__ double ddiv(double a, const StageParams& p, int axis)
 #endif
 }
 
+// Fused halo exchange of a decomposed run whose march axis is split: a cell
+// of the first / last g march rows is also stored into the ghost rows of the
+// low / high neighbour's copy of the same buffer (peer memory over NVLink),
+// so the next stage reads its halo without a separate exchange
+// (parallel.py:201-254; the transverse crop of solver.py:99-104 means the
+// face layers suffice).  A no-op outside such runs (null peers).
+__device__ __forceinline__ void peer_store(const StageParams& p, int64_t o, int64_t row, int64_t cstride, int c,
+                                           double v) {
+  if (p.peer_lo && row < p.g) p.peer_lo[o + p.peer_shift + c * cstride] = v;
+  if (p.peer_hi && row >= p.n_march - p.g) p.peer_hi[o - p.peer_shift + c * cstride] = v;
+}
+
 // RK stage combination (solver.py:166-173)
 __device__ __forceinline__ double rk_combine(int kind, double un, double us, double dt, double L) {
 #if FVB_FAST
@@ -1017,7 +1029,10 @@ ring_kernel(const StageParams p) {
           const int o = co + roff(r - 1);
           if constexpr (NI == 1) {
 #pragma unroll
-            for (int c = 0; c < NC; ++c) out[o + c * cs] = v[c];
+            for (int c = 0; c < NC; ++c) {
+              out[o + c * cs] = v[c];
+              peer_store(p, o, r - 1, cs, c, v[c]);
+            }
             if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v, xf, r - 1, 0, smax);
           } else {
 #pragma unroll
@@ -1415,12 +1430,18 @@ pair_kernel(const StageParams p) {
           const int o = roff(r - 1);
           if (cell0) {
 #pragma unroll
-            for (int c = 0; c < NC; ++c) out[co0 + o + c * cs] = v0[c];
+            for (int c = 0; c < NC; ++c) {
+              out[co0 + o + c * cs] = v0[c];
+              peer_store(p, co0 + o, r - 1, cs, c, v0[c]);
+            }
             if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v0, f0, r - 1, 0, smax);
           }
           if (cell1) {
 #pragma unroll
-            for (int c = 0; c < NC; ++c) out[co1 + o + c * cs] = v1[c];
+            for (int c = 0; c < NC; ++c) {
+              out[co1 + o + c * cs] = v1[c];
+              peer_store(p, co1 + o, r - 1, cs, c, v1[c]);
+            }
             if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v1, f0 + 1, r - 1, 0, smax);
           }
         }
@@ -1635,7 +1656,10 @@ ring3_kernel(const StageParams p) {
           if (cell) {
             const int64_t o = co + roff(r - 1);
 #pragma unroll
-            for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
+            for (int c = 0; c < NC; ++c) {
+              out[o + c * p.sc] = v[c];
+              peer_store(p, o, r - 1, p.sc, c, v[c]);
+            }
             if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v, xf, yf, r - 1, smax);
           }
         }
@@ -1908,7 +1932,10 @@ ring3i_kernel(const StageParams p) {
           if (cell) {
             const int64_t o = co + roff(r - 1);
 #pragma unroll
-            for (int c = 0; c < NC; ++c) out[o + c * p.sc] = v[c];
+            for (int c = 0; c < NC; ++c) {
+              out[o + c * p.sc] = v[c];
+              peer_store(p, o, r - 1, p.sc, c, v[c]);
+            }
             if constexpr (FIN) post_cell<EQ, DIM, NC>(p, st, v, xf, yf, r - 1, smax);
           }
         }

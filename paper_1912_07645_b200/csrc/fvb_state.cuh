@@ -195,6 +195,10 @@ struct StageParams {
   int64_t row_hi;     // (inner box / shell slabs of the overlap schedule, parallel.py:288-361)
   int64_t x_lo, x_hi; // in-plane cell ranges of this launch (x; y in 3D): the inner box / shells of
   int64_t y_lo, y_hi; // a split in-plane axis.  Honoured by the ring, pair and 3D all-interior kernels.
+  double* peer_lo;    // fused halo exchange (decomposed run, march axis split): the low / high
+  double* peer_hi;    // neighbour's copy of `out` (peer memory, interior origin); cells of the first /
+  int64_t peer_shift; // last g march rows are also stored there, shifted by n_march * march stride
+  int64_t n_march;
   unsigned nblocks;   // blocks per state (finalize counter)
   int shared_state;   // 1: all instances are subdomains of one run (one FvbState)
   int defer_finalize; // 1: leave maxima/flags in the state; the caller reduces them

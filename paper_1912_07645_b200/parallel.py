@@ -459,11 +459,20 @@ class DecomposedRun:
     stages the exchanged slabs and the reduce through host memory (gloo),
     e.g. to test several ranks on one GPU.
 
+    ``peer_halos`` (NCCL groups, march axis the only split axis, one GPU per
+    rank): the fused halo exchange -- the three field buffers live in
+    symmetric memory (torch.distributed._symmetric_memory, NVLink peer
+    mappings), every stage kernel also stores its first / last g march rows
+    into the neighbours' ghost rows (``fvb_run_set_peers``), and a device
+    barrier after each stage orders the ranks; no pack, no NCCL message per
+    stage.  "auto" uses it when available.
+
     ``advance(n)`` enqueues up to n more steps; ``finish()`` returns
     (DeviceField of the final subdomain, [RankRecord])."""
 
     def __init__(self, local, cfg, topo: RankTopology, n_steps=None, *, arith=None, group=None,
-                 cpu_comm: bool = False, overlap: bool = True, poll_every: int = 64, log: bool = True):
+                 cpu_comm: bool = False, overlap: bool = True, poll_every: int = 64, log: bool = True,
+                 peer_halos="auto"):
         import torch
         import torch.distributed as dist
 
@@ -476,11 +485,23 @@ class DecomposedRun:
             dev = local if isinstance(local, DeviceField) else DeviceField.from_host(local)
             self.grid, self.ncomp = dev.grid, dev.ncomp
             grid = self.grid
-            b0 = dev.data.unsqueeze(0).contiguous()
-            self.bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
-            self.ctx = ctx = N.context()
             self.split = tuple(k for k in range(grid.dim) if topo.ranks_per_axis[k] > 1)
             self.periodic = [int(_v(cfg.bc[k]) == "periodic") for k in range(grid.dim)]
+            self.march = grid.dim - 1
+            self.symm = None
+            if self._peer_ok(peer_halos, cpu_comm):
+                import torch.distributed._symmetric_memory as symm_mem
+
+                # the three RK buffers in one symmetric allocation: every rank
+                # maps its neighbours' copies (same layout, same offsets)
+                block = symm_mem.empty((3, 1) + tuple(dev.data.shape), dtype=torch.float64, device="cuda")
+                self.symm = symm_mem.rendezvous(block, group or dist.group.WORLD)
+                block[0, 0].copy_(dev.data)
+                self.bufs = [block[k] for k in range(3)]
+            else:
+                b0 = dev.data.unsqueeze(0).contiguous()
+                self.bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
+            self.ctx = ctx = N.context()
             ctx.check(ctx.lib.fvb_run_set_external_reduce(ctx.h, 1))
             mode = N.MODE_FIXED if n_steps is not None else N.MODE_PAR_T_END
             self.run = DeviceRun(grid, cfg, self.bufs, 1, mode, n_steps, arith, halo_axes=self.split, ctx=ctx,
@@ -489,8 +510,9 @@ class DecomposedRun:
             self.cpu_comm = cpu_comm
             self.red = torch.zeros(grid.dim + 2, dtype=torch.float64, device="cuda")
             self.red_host = torch.zeros(grid.dim + 2, dtype=torch.float64, pin_memory=True) if cpu_comm else None
-            self.march = grid.dim - 1
             self.g = grid.ghost_width
+            if self.symm is not None:
+                self._set_peers()
             # overlap schedule: every split axis long enough for an inner box
             self.ovl = overlap and grid.dim >= 2 and bool(self.split) and \
                 all(grid.cells[a] > 2 * self.g for a in self.split)
@@ -501,6 +523,40 @@ class DecomposedRun:
             self._tic = time.perf_counter()
             self._last = 0
             self._reduce_and_finalize(0)
+
+    def _peer_ok(self, peer_halos, cpu_comm) -> bool:
+        """Fused halo exchange applicable: asked for (or auto), NCCL group,
+        only the march axis split, symmetric memory available."""
+        if not peer_halos or cpu_comm or self.split != (self.march,) or self.march == 0:
+            return False
+        if self.dist.get_backend(self.group) != "nccl":
+            return False
+        try:
+            import torch.distributed._symmetric_memory  # noqa: F401
+        except Exception:
+            if peer_halos == "auto":
+                return False
+            raise
+        return True
+
+    def _set_peers(self):
+        """Neighbours' buffer pointers (symmetric memory) -> fvb_run_set_peers."""
+        ctx = self.ctx
+        nbytes = self.bufs[0].numel() * 8
+        base = int(getattr(self.symm, "offset", 0) or 0)  # the block's offset in each rank's allocation
+        ptrs = [int(q) + base for q in self.symm.buffer_ptrs]
+        per = bool(self.periodic[self.march])
+        lo = self.topo.neighbor(self.rank, self.march, 0, per)
+        hi = self.topo.neighbor(self.rank, self.march, 1, per)
+
+        def arr(r):
+            if r is None:
+                return None
+            return (N.C.c_void_p * 3)(*[N.C.c_void_p(int(ptrs[r]) + k * nbytes) for k in range(3)])
+
+        self._peer_arrays = (arr(lo), arr(hi))  # keep alive
+        ctx.check(ctx.lib.fvb_run_set_peers(ctx.h, self._peer_arrays[0], self._peer_arrays[1]))
+        self._peer_primed = False  # the first stage input's ghosts come from one regular exchange
 
     def _reduce_and_finalize(self, post: int):
         ctx, dist, red = self.ctx, self.dist, self.red
@@ -544,6 +600,14 @@ class DecomposedRun:
     def _stage(self, st, u):
         ctx, dist, topo, rank, per, grp = self.ctx, self.dist, self.topo, self.rank, self.periodic, self.group
         pack, unpack, alloc = self.halos.movers(u)
+        if self.symm is not None:
+            if not self._peer_primed:  # ghosts of the very first stage input
+                halo_exchange_dist(topo, rank, per, pack, unpack, alloc, dist, grp)
+                self._peer_primed = True
+            self._outflow_edges(u, self.split)
+            ctx.check(ctx.lib.fvb_run_stage(ctx.h, st))  # also stores the neighbours' ghost rows
+            self.symm.barrier(channel=0)  # every rank's stage (and its peer stores) done
+            return
         if not self.ovl:
             halo_exchange_dist(topo, rank, per, pack, unpack, alloc, dist, grp)
             self._outflow_edges(u, self.split)
