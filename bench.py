@@ -494,7 +494,9 @@ def bench_kh3d(args, env):
     dev = DeviceField(local, 5, buf[0])
     total = args.warmup + args.steps
     run = DecomposedRun(dev, cfg, topo, n_steps=total + 1, arith=args.arith, group=None, log=False,
-                        poll_every=1 << 30)
+                        poll_every=1 << 30, peer_halos={"auto": "auto", "peer": True, "nccl": False}[args.halo])
+    halo_path = ("fused peer stores (symmetric memory over NVLink) + device barrier per stage"
+                 if run.symm is not None else "NCCL P2P messages, inner box overlapped")
     run.advance(args.warmup)
     with Clocks(env.dev_index) as clk:
         l0 = run.ctx.launches()
@@ -536,7 +538,7 @@ def bench_kh3d(args, env):
     return {"value": value, "ms_per_step": ms_per_step, "roofline": roof, "e2e": e2e, "launches": launches,
             "clocks": clk.summary(), "t_start": 0.0, "stats": None,
             "state": f"KH3D from t = 0 after {args.warmup} warm-up steps",
-            "parallelism": f"z-slab decomposition x{ws} (NCCL halos, overlapped inner box)" if ws > 1
+            "parallelism": f"z-slab decomposition x{ws}, halos: {halo_path}" if ws > 1
             else "single GPU (one-rank group: same code path)",
             "scaling": "weak"}
 
@@ -729,6 +731,8 @@ def main():
     ap.add_argument("--mc-steps", type=int, default=20, help="mc: RK3 steps per sample (run_mc max_steps)")
     ap.add_argument("--workers", type=int, default=max(1, min(16, os.cpu_count() or 1)),
                     help="mc e2e: host threads evaluating the numpy initial data")
+    ap.add_argument("--halo", default="auto", choices=["auto", "peer", "nccl"],
+                    help="kh3d: fused peer-memory halo stores (auto when symmetric memory works) or NCCL messages")
     ap.add_argument("--cpu-steps", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--e2e-reps", type=int, default=3)

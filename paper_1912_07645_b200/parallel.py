@@ -490,15 +490,27 @@ class DecomposedRun:
             self.march = grid.dim - 1
             self.symm = None
             if self._peer_ok(peer_halos, cpu_comm):
-                import torch.distributed._symmetric_memory as symm_mem
+                try:
+                    import torch.distributed._symmetric_memory as symm_mem
 
-                # the three RK buffers in one symmetric allocation: every rank
-                # maps its neighbours' copies (same layout, same offsets)
-                block = symm_mem.empty((3, 1) + tuple(dev.data.shape), dtype=torch.float64, device="cuda")
-                self.symm = symm_mem.rendezvous(block, group or dist.group.WORLD)
-                block[0, 0].copy_(dev.data)
-                self.bufs = [block[k] for k in range(3)]
-            else:
+                    # the three RK buffers in one symmetric allocation: every rank
+                    # maps its neighbours' copies (same layout, same offsets)
+                    block = symm_mem.empty((3, 1) + tuple(dev.data.shape), dtype=torch.float64, device="cuda")
+                    hdl = symm_mem.rendezvous(block, group or dist.group.WORLD)
+                    base = int(getattr(hdl, "offset", 0) or 0)
+                    if int(hdl.buffer_ptrs[self.rank]) + base != block.data_ptr():
+                        raise RuntimeError("symmetric buffer pointers do not match the local block")
+                    self.symm = hdl
+                    block[0, 0].copy_(dev.data)
+                    self.bufs = [block[k] for k in range(3)]
+                except Exception as exc:  # no peer mappings here: the NCCL exchange instead
+                    if peer_halos is True:
+                        raise
+                    import warnings
+
+                    warnings.warn(f"fused peer halos unavailable ({exc}); using NCCL halo messages")
+                    self.symm = None
+            if self.symm is None:
                 b0 = dev.data.unsqueeze(0).contiguous()
                 self.bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
             self.ctx = ctx = N.context()

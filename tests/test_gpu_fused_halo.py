@@ -17,6 +17,19 @@ pytestmark = pytest.mark.gpu
 
 
 def _fused_run(P, init, cfg, nrank, n_steps, arith):
+    """All subdomains' contexts on ONE explicit stream (the legacy default
+    stream would give each context its own stream: no ordering between
+    them)."""
+    import torch
+
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        out = _fused_run_on_stream(P, init, cfg, nrank, n_steps, arith)
+    torch.cuda.current_stream().wait_stream(stream)
+    return out
+
+
+def _fused_run_on_stream(P, init, cfg, nrank, n_steps, arith):
     import torch
 
     from paper_1912_07645_b200 import _native as N
