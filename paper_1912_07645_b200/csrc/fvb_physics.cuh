@@ -29,6 +29,9 @@
 #ifndef FVB_WARP_SKIP
 #define FVB_WARP_SKIP 0
 #endif
+#ifndef FVB_FAST_NO_EQ
+#define FVB_FAST_NO_EQ 1
+#endif
 
 namespace fvb {
 
@@ -581,7 +584,11 @@ __device__ __forceinline__ void interface_flux_lazy(const double* uL0, const dou
       uL[c] = uL0[c];
       uR[c] = uR0[c];
     }
-    bool equal = bits_equal_all<NC>(uL, uR);
+    // uL == uR -> fL (numerics.py:195-196).  The fast mode without the warp
+    // shortcuts skips the test: for bitwise-equal states the general HLLC
+    // formula returns f(u) up to rounding, and equal inputs give equal
+    // fluxes, so uniform regions still have an exactly zero residual.
+    bool equal = (FVB_FAST && !FVB_WARP_SKIP && FVB_FAST_NO_EQ) ? false : bits_equal_all<NC>(uL, uR);
     const unsigned am = __activemask();
     if (FVB_WARP_SKIP && !__any_sync(am, !equal)) {
       // Whole warp on uniform states (the KH bands): F(u, u) = f(u) for
@@ -618,7 +625,7 @@ __device__ __forceinline__ void interface_flux_lazy(const double* uL0, const dou
         cells(uL, uR);
         L = euler_state<DIM>(uL, axis, P);
         R = euler_state<DIM>(uR, axis, P);
-        equal = bits_equal_all<NC>(uL, uR);
+        equal = (FVB_FAST && !FVB_WARP_SKIP && FVB_FAST_NO_EQ) ? false : bits_equal_all<NC>(uL, uR);
       }
     }
     if constexpr (FLUX == FLUX_HLLC) hllc<DIM>(uL, uR, L, R, axis, P, F, errbits, equal);
