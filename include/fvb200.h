@@ -202,6 +202,10 @@ int64_t fvb_launch_count(const fvb_ctx* ctx);
  * dense (ncomp, *interior) arrays. */
 int fvb_moments_push(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay,
                      const double* u, int inst, double* mean, double* m2, int64_t count_before);
+/* the same for instances inst .. inst+nbatch-1 merged in that order (one
+ * read + write of mean / m2 per batch; bitwise equal to nbatch pushes) */
+int fvb_moments_push_batch(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, const double* u, int inst,
+                           int nbatch, double* mean, double* m2, int64_t count_before);
 
 /* uq.py:135-148 merge of two accumulators (Chan) for the cross-GPU reduce:
  * (mean_a, m2_a, count_a) <- merge with (mean_b, m2_b, count_b), n values. */

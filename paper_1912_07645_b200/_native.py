@@ -89,6 +89,8 @@ _SIGS = {
     "fvb_launch_count": ([C.c_void_p], C.c_int64),
     "fvb_moments_push": ([C.c_void_p, C.POINTER(Scheme), C.POINTER(Layout), C.c_void_p, C.c_int,
                           C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
+    "fvb_moments_push_batch": ([C.c_void_p, C.POINTER(Scheme), C.POINTER(Layout), C.c_void_p, C.c_int, C.c_int,
+                                C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
     "fvb_moments_merge": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                            C.c_int64, C.c_int64], C.c_int),
     "fvb_structure_push": ([C.c_void_p, C.POINTER(Scheme), C.POINTER(Layout), C.c_void_p, C.c_int, C.c_int,

@@ -114,17 +114,24 @@ __global__ void halo_kernel(Pad p, fvb_layout L, double* u, int ncomp, int axis,
   }
 }
 
-// One sample merged into (mean, m2) holding `count` samples.  The sample is
-// a fresh MomentAccumulator after update(v) (uq.py:125-133 with count 0):
+// Samples inst .. inst+nbatch-1 merged, in that order, into (mean, m2)
+// holding `count` samples.  Each sample is a fresh MomentAccumulator after
+// update(v) (uq.py:125-133 with count 0):
 //   om = 0 + (v - 0)/1,  om2 = 0 + (v - 0)*(v - om)
-// merged by uq.py:135-148 (first merge copies).
-__global__ void moments_push_kernel(Pad p, fvb_layout L, const double* u, int ncomp, int inst, double* mean,
-                                    double* m2, long long count) {
+// merged by uq.py:135-148 (the first merge copies).  The running (mean, m2)
+// of an element stay in registers across the batch: the statistics cost
+// one read + one write of (mean, m2) per BATCH instead of per sample, with
+// the exact operation sequence of nbatch single merges (bitwise equal).
+constexpr int kMomMaxBatch = 64;
+
+__global__ void moments_push_kernel(Pad p, fvb_layout L, const double* u, int ncomp, int inst, int nbatch,
+                                    double* mean, double* m2, long long count) {
+  __shared__ double fracs[kMomMaxBatch];  // other.count / total (int / int) of merge b
+  for (int b = threadIdx.x; b < nbatch; b += blockDim.x) fracs[b] = 1.0 / (double)(count + b + 1);
+  __syncthreads();
   // block-strided over (component, z, y) rows, threads over x: no per-element
   // index division; the (mean, m2) arrays are dense (ncomp, z, y, x)
   const int64_t nrow = p.n[1] * p.n[2];
-  const double frac = 1.0 / (double)(count + 1);   // other.count / total (int / int)
-  const double fc = (double)count;
   for (int64_t row = blockIdx.x; row < nrow * ncomp; row += gridDim.x) {
     const int c = (int)(row / nrow);
     const int64_t yz = row - (int64_t)c * nrow;
@@ -133,19 +140,29 @@ __global__ void moments_push_kernel(Pad p, fvb_layout L, const double* u, int nc
     double* mrow = mean + row * p.n[0];
     double* qrow = m2 + row * p.n[0];
     for (int64_t x = threadIdx.x; x < p.n[0]; x += blockDim.x) {
-      const double v = src[x];
-      const double d0 = v - 0.0;
-      const double om = 0.0 + d0 / 1.0;
-      const double om2 = 0.0 + d0 * (v - om);
-      if (count == 0) {
-        mrow[x] = om;
-        qrow[x] = om2;
-      } else {
-        const double mu = mrow[x];
-        const double delta = om - mu;
-        mrow[x] = mu + delta * frac;
-        qrow[x] = (qrow[x] + om2) + ((delta * delta) * fc) * frac;
+      double mu = 0.0, q = 0.0;
+      if (count > 0) {
+        mu = mrow[x];
+        q = qrow[x];
       }
+      for (int b = 0; b < nbatch; ++b) {
+        const double v = src[b * L.si + x];
+        const double d0 = v - 0.0;
+        const double om = 0.0 + d0 / 1.0;
+        const double om2 = 0.0 + d0 * (v - om);
+        if (count + b == 0) {
+          mu = om;
+          q = om2;
+        } else {
+          const double frac = fracs[b];
+          const double fc = (double)(count + b);
+          const double delta = om - mu;
+          mu = mu + delta * frac;
+          q = (q + om2) + ((delta * delta) * fc) * frac;
+        }
+      }
+      mrow[x] = mu;
+      qrow[x] = q;
     }
   }
 }
@@ -469,12 +486,14 @@ int launch_halo_instances(const fvb_scheme& s, const fvb_layout& L, double* u, i
   return 1;
 }
 
-int launch_moments_push(const fvb_scheme& s, const fvb_layout& L, const double* u, int inst, double* mean,
+int launch_moments_push(const fvb_scheme& s, const fvb_layout& L, const double* u, int inst, int nbatch, double* mean,
                         double* m2, int64_t count_before, cudaStream_t st) {
   const Pad p = make_pad(s);
   const int64_t rows = p.n[1] * p.n[2] * s.ncomp;
   const int blocks = (int)std::min<int64_t>(rows, 148 * 16);
-  moments_push_kernel<<<blocks, 256, 0, st>>>(p, L, u, s.ncomp, inst, mean, m2, (long long)count_before);
+  for (int b0 = 0; b0 < nbatch; b0 += kMomMaxBatch)
+    moments_push_kernel<<<blocks, 256, 0, st>>>(p, L, u, s.ncomp, inst + b0, std::min(kMomMaxBatch, nbatch - b0), mean,
+                                                m2, (long long)count_before + b0);
   return 0;
 }
 

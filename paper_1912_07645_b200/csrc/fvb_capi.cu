@@ -40,7 +40,7 @@ int launch_fill_axis(const fvb_scheme& s, const fvb_layout& L, double* u, int ni
 int launch_halo(const fvb_scheme& s, const fvb_layout& L, double* u, int axis, int side, double* buf,
                 int unpack, cudaStream_t st);
 int64_t halo_count(const fvb_scheme& s, int axis);
-int launch_moments_push(const fvb_scheme& s, const fvb_layout& L, const double* u, int inst, double* mean,
+int launch_moments_push(const fvb_scheme& s, const fvb_layout& L, const double* u, int inst, int nbatch, double* mean,
                         double* m2, int64_t count_before, cudaStream_t st);
 int launch_moments_merge(double* ma, double* m2a, int64_t ca, const double* mb, const double* m2b, int64_t cb,
                          int64_t n, cudaStream_t st);
@@ -986,8 +986,14 @@ int fvb_run(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, double* bu
 
 int fvb_moments_push(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, const double* u, int inst,
                      double* mean, double* m2, int64_t count_before) {
-  fvb::launch_moments_push(*s, *lay, u, inst, mean, m2, count_before, ctx->stream);
-  ctx->launches++;
+  return fvb_moments_push_batch(ctx, s, lay, u, inst, 1, mean, m2, count_before);
+}
+
+int fvb_moments_push_batch(fvb_ctx* ctx, const fvb_scheme* s, const fvb_layout* lay, const double* u, int inst,
+                           int nbatch, double* mean, double* m2, int64_t count_before) {
+  if (nbatch < 1) return set_err(ctx, FVB_E_CONFIG, "nbatch must be >= 1");
+  fvb::launch_moments_push(*s, *lay, u, inst, nbatch, mean, m2, count_before, ctx->stream);
+  ctx->launches += (nbatch + 63) / 64;
   return check_launch(ctx, "moments_push");
 }
 

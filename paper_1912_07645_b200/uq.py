@@ -163,6 +163,16 @@ class FieldMoments:
                                            N.C.c_void_p(self._m2.data_ptr()), self.count))
         self.count += 1
 
+    def push_device_batch(self, ctx, scheme, layout, buf, inst: int, n: int):
+        """Merge instances inst .. inst+n-1 of ``buf`` in that order: one
+        kernel, (mean, M2) read and written once (bitwise equal to n pushes)."""
+        self._alloc()
+        ctx.check(ctx.lib.fvb_moments_push_batch(ctx.h, N.C.byref(scheme), N.C.byref(layout),
+                                                 N.C.c_void_p(buf.data_ptr()), inst, int(n),
+                                                 N.C.c_void_p(self._mean.data_ptr()),
+                                                 N.C.c_void_p(self._m2.data_ptr()), self.count))
+        self.count += int(n)
+
     def update(self, field) -> None:
         """FieldMoments.update (uq.py:174-175) for one field."""
         dev = field if isinstance(field, DeviceField) else DeviceField.from_host(field)
@@ -542,10 +552,13 @@ def _ensemble(plan, level, grid, cfg, evaluate_init, slots, lo, hi, batch=None, 
                         _raise_run_error(info, grid, ncomp)
                     except E.ConslawError as exc:
                         raise E.SimulationError(f"{where}sample {j} failed: {exc}") from exc
-            for i, j in enumerate(ks):
-                buf = bufs[int(infos[i].steps) % 2] if cfg.rk_order == 1 else bufs[0]
-                for s in slots:
-                    s.push(ctx, desc, layout, buf, i, grid, ncomp, like)
+            where_ = [int(infos[i].steps) % 2 if cfg.rk_order == 1 else 0 for i in range(len(ks))]
+            for s in slots:  # each slot sees the batch's samples in sample order
+                if isinstance(s.gpu, FieldMoments) and len(set(where_)) == 1:
+                    s.gpu.push_device_batch(ctx, desc, layout, bufs[where_[0]], 0, len(ks))  # one kernel per batch
+                    continue
+                for i in range(len(ks)):
+                    s.push(ctx, desc, layout, bufs[where_[i]], i, grid, ncomp, like)
     if evals:
         evals.shutdown()
 
