@@ -33,6 +33,9 @@ def algorithmic(cap, name):
         stage = 2 if "<0, 1, 1, 0>" in name and False else None
         return None, "see ring3 note"
     if "moments_push" in name:
+        if cap == "mc_moments":   # batched push: 16 samples read, (mean, M2) read + written once
+            return 16 * 512 * 512 * 4 * 8 + 512 * 512 * 4 * 32, \
+                "16 samples x 512^2 cells x 4 comps x 8 B read + (mean, M2) rmw 32 B once per batch"
         if cap == "bqmc_stats":
             return 2048 * 2048 * 40, "2048^2 cells x (r u 8 + rmw mean 16 + rmw M2 16) B"
         return 512 * 512 * 4 * 40, "512^2 cells x 4 comps x (r u 8 + rmw mean 16 + rmw M2 16) B"
