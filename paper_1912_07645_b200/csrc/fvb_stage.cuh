@@ -1843,31 +1843,32 @@ ring3i_kernel(const StageParams p) {
   const int64_t ra = p.row_lo + (int64_t)chunk * p.H;
   const int64_t rb = min(ra + (int64_t)p.H, p.row_hi);
   const int64_t mxf = map_index(xf, p.n[0], p.bc[0], p.g);
-  const int64_t co = mxf + map_index(yf, p.n[1], p.bc[1], p.g) * p.sy;
+  const int co = (int)(mxf + map_index(yf, p.n[1], p.bc[1], p.g) * p.sy);  // < 2^31 (validated)
   // extra copies: lanes 0 / NT-1 the x-halo columns of their row; warps 0, 1 /
   // NTY-2, NTY-1 one y-halo row each (ring rows 0, 1 / WY-2, WY-1), interior columns
+  // (as 32-bit deltas from co: an instance component spans < 2^31 elements,
+  // and two int32 registers instead of two int64 pairs keep the loop spill-free)
   const bool hx_t = tx == 0 || tx == NT - 1;
-  const int64_t hxo = map_index(tx == 0 ? x0 - 2 : x0 + NT - 1, p.n[0], p.bc[0], p.g) +
-                      map_index(yf, p.n[1], p.bc[1], p.g) * p.sy;
+  const int dxh = (int)(map_index(tx == 0 ? x0 - 2 : x0 + NT - 1, p.n[0], p.bc[0], p.g) - mxf);
   const int hxc = tx == 0 ? 0 : W - 1;
   const bool hy_t = ty <= 1 || ty >= NTY - 2;
   const int hyr = ty <= 1 ? ty : WY - NTY + ty;  // ring row 0, 1 | WY-2, WY-1
-  const int64_t hyo = mxf + map_index(y0 - 2 + hyr, p.n[1], p.bc[1], p.g) * p.sy;
+  const int dyh = (int)((map_index(y0 - 2 + hyr, p.n[1], p.bc[1], p.g) - map_index(yf, p.n[1], p.bc[1], p.g)) * p.sy);
   const int tid = ty * NT + tx;
   for (int i = tid; i < p.H + 4; i += NT * NTY) rtab[i] = (int)(map_index(ra - 2 + i, p.n[2], p.bc[2], p.g) * p.sz);
   __syncthreads();
-  auto roff = [&](int64_t r) -> int64_t { return rtab[r - (ra - 2)]; };
+  auto roff = [&](int64_t r) -> int { return rtab[r - (ra - 2)]; };
   auto fetch = [&](int64_t r, int slot) {
-    const int64_t ro = roff(r);
+    const int ro = roff(r);
 #pragma unroll
-    for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, ty + 2, tx + 1), us + co + ro + c * p.sc);
+    for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, ty + 2, tx + 1), us + (co + ro) + c * p.sc);
     if (hx_t) {
 #pragma unroll
-      for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, ty + 2, hxc), us + hxo + ro + c * p.sc);
+      for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, ty + 2, hxc), us + (co + dxh + ro) + c * p.sc);
     }
     if (hy_t) {
 #pragma unroll
-      for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, hyr, tx + 1), us + hyo + ro + c * p.sc);
+      for (int c = 0; c < NC; ++c) cp_async8(&RG(slot, c, hyr, tx + 1), us + (co + dyh + ro) + c * p.sc);
     }
   };
 
@@ -1930,7 +1931,7 @@ ring3i_kernel(const StageParams p) {
             v[c] = KS == 0 ? Lc : rk_combine(p.kind, UN ? unc[UN ? c : 0] : 0.0, A[c], dt, Lc);
           }
           if (cell) {
-            const int64_t o = co + roff(r - 1);
+            const int o = co + roff(r - 1);
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
               out[o + c * p.sc] = v[c];
@@ -1948,7 +1949,7 @@ ring3i_kernel(const StageParams p) {
     if (r >= ra && r < rb) {
       if constexpr (UN) {
         if (cell) {  // u^n of plane r for the next iteration's finish
-          const int64_t o = co + roff(r);
+          const int o = co + roff(r);
 #pragma unroll
           for (int c = 0; c < NC; ++c) unc[c] = un[o + c * p.sc];
         }

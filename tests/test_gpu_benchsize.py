@@ -6,7 +6,10 @@
 * KH2D 1024^2 fast mode from that state after 1, 3 and 10 steps: relative
   L1 <= 1e-12 per component (sum|a-b| / sum|b| of each conserved
   component, no floor), dt within 1e-12.
-* KH3D 128^3 (C4 shape), exact, 1 step: bitwise.
+* KH3D 128^3 (C4 shape), exact, 1 step: bitwise; and from a developed state
+  with flow along all three axes (t = 0.5, averaged with its y<->z
+  transpose): exact 1 step bitwise, fast after 1 and 3 steps <= 1e-12 per
+  component.
 * C3: run_mc over 16 KH2D samples at 512^2 and C5: 4 Burgers QMC samples at
   2048^2 (truncated t_end, two steps each), exact mode: moments bitwise equal
   to the sequential sample-order merge of the oracle's per-sample finals,
@@ -33,6 +36,7 @@ KH_SCHEME = dict(eq="euler", flux="hllc", recon="weno2", rk=3, cfl=0.475, t_end=
 C3_TEND = 4.0e-4   # dt_1 ~ 2.19e-4 at 512^2: two steps
 C5_TEND = 1.5e-4   # dt_1 ~ 7.7e-5 at 2048^2: two steps
 FAST_CHECKPOINTS = (1, 3, 10)
+KH3D_CHECKPOINTS = (1, 3)
 
 
 def rel_l1_components(a, b):
@@ -99,6 +103,18 @@ def jobs(P, pool):
     f["kh_t1"] = pool.submit(J.simulate_checkpoints, state.data, s2, (2,))
     for k in FAST_CHECKPOINTS:  # separate jobs: they run side by side
         f[f"kh_t1_{k}"] = pool.submit(J.simulate_checkpoints, state.data, s2, (k,))
+    # a developed 3D state with flow in all three directions: KH3D 128^3 run
+    # to t = 0.5 on the GPU (z-uniform, vz = 0 -- the preset is extruded), then
+    # averaged with its y<->z transpose (axes and momenta swapped): a convex
+    # combination of physical states, non-trivial along every axis
+    g3, c3cfg = _kh_objects(P, 128, dim=3)
+    st3, _ = P.run_simulation(kelvin_helmholtz(g3, KH_VEC),
+                              P.SchemeConfig(c3cfg.model, c3cfg.flux, c3cfg.recon, 3, 0.475, 0.5), arith="fast")
+    d = st3.data
+    mix = np.ascontiguousarray(0.5 * (d + d.transpose(0, 2, 1, 3)[[0, 1, 3, 2, 4]]))
+    f["state3"] = mix
+    for k in KH3D_CHECKPOINTS:
+        f[f"kh3d_mix_{k}"] = pool.submit(J.simulate_checkpoints, mix, s3, (k,))
     return f
 
 
@@ -202,3 +218,26 @@ def test_kh3d_128_fast_one_step(P, jobs):
     ref, dts = jobs["kh3d"].result()[1]
     assert rel_l1_field(out.interior, ref) <= 1e-12
     assert abs(recs[0].dt - dts[0]) <= 1e-12 * dts[0]
+
+
+def test_kh3d_128_exact_from_developed_3d_state(P, jobs):
+    """KH3D 128^3 exact mode, 1 step from the developed three-direction state:
+    bitwise equal to the oracle (fields and dt)."""
+    grid, cfg = _kh_objects(P, 128, dim=3)
+    out, recs = P.run_simulation(P.Field(grid, 5, jobs["state3"].copy()), cfg, max_steps=1, arith="exact")
+    ref, dts = jobs["kh3d_mix_1"].result()[1]
+    assert [r.dt for r in recs] == dts
+    assert O.sha16(out.interior) == O.sha16(ref), "KH3D 128^3 exact differs from the oracle (developed state)"
+
+
+@pytest.mark.parametrize("steps", KH3D_CHECKPOINTS)
+def test_kh3d_128_fast_from_developed_3d_state(P, jobs, steps):
+    """The fast 3D default (ring3i) from the developed three-direction state:
+    relative L1 <= 1e-12 per conserved component, no floor (every momentum
+    component is O(1) here), dt within 1e-12."""
+    grid, cfg = _kh_objects(P, 128, dim=3)
+    out, recs = P.run_simulation(P.Field(grid, 5, jobs["state3"].copy()), cfg, max_steps=steps, arith="fast")
+    ref, dts = jobs[f"kh3d_mix_{steps}"].result()[steps]
+    err = rel_l1_components(out.interior, ref)
+    assert err <= 1e-12, f"fast mode relative L1 {err:.3e} after {steps} steps"
+    assert max(abs(r.dt - d) / d for r, d in zip(recs, dts)) <= 1e-12
