@@ -47,16 +47,22 @@ def test_run_simulation_exact_bitwise(P, golden, golden_arrays, name):
     assert O.sha16(final.data) == case["data_sha"], case["name"]
 
 
-@pytest.mark.parametrize("name", ["kh2d64_weno2_50", "kh2d32_weno3_20", "kh3d16_weno2_5", "euler2d_hllc_weno3_outflow",
-                                  "euler3d_rusanov_weno2_outflow", "burgers2d64_qmc0", "double_rarefaction",
-                                  "sod400_preset", "advection2d_weno3_rk3"])
+@pytest.mark.parametrize("name", GOLDEN_RUN_NAMES)
 def test_run_simulation_fast_tolerance(P, golden, golden_arrays, name):
+    """Every golden run (1D/2D/3D, Euler/Burgers/advection, all fluxes,
+    reconstructions, RK orders and boundaries) in fast arithmetic -- the
+    fast-mode default kernels (pair in 2D, ring3i in 3D) -- against the
+    reference's final field."""
     case = next(r for r in golden["runs"] if r["name"] == name)
     grid, cfg = product_objects(case["scheme"])
     init = _init_field(P, case, golden_arrays, grid)
     final, recs = P.run_simulation(init, cfg, max_steps=case["max_steps"], arith="fast")
-    ref = golden_arrays[name + "__final"]
     sc = oracle_scheme(case["scheme"])
+    if name + "__final" in golden_arrays:
+        ref = golden_arrays[name + "__final"]
+    else:  # only the SHA is stored: the golden-pinned oracle recomputes the final field
+        ref, _ = O.simulate(np.array(init.data), sc, case["max_steps"])
+        assert O.sha16(O.interior(ref, sc)) == case["final_sha"], name
     ref_in = O.interior(ref, sc)
     assert len(recs) == case["steps"], name
     err = rel_l1_field(final.interior, ref_in)
