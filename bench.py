@@ -243,6 +243,14 @@ def _profile_json(name):
         return None
 
 
+def _traffic_key(roof, name):
+    """ncu DRAM bytes per stage launch of the same kernel and workload (profiles/)."""
+    t = _profile_json(name)
+    if t:
+        roof["traffic"] = t.get("stage_bytes_per_launch")
+        roof["traffic_source"] = t.get("source")
+
+
 def _kh2d_profile_keys(roof):
     """traffic (ncu dram bytes per stage launch) and the FP64 roof from the
     committed captures of the same kernel (profiles/)."""
@@ -355,11 +363,38 @@ def bench_single(args, env):
     roof = _roofline(bps, cells * 3 * args.steps, t_ms * 1e-3, kname + " (3 launches/step)")
     if not burgers:
         _kh2d_profile_keys(roof)
+    else:
+        _traffic_key(roof, "traffic_bqmc.json")
 
     # e2e through the public API with host buffers, from the same developed
     # state the kernel timing starts at: run_simulation(host Field) with the
     # input in pinned memory (and, beside it, a pageable numpy Field)
     e2e = None
+    if burgers:
+        # e2e: the reference-facing run_mc with the caller's host numpy
+        # initial data (H2D of every sample) and the statistics read back
+        from paper_1912_07645_b200 import uq
+
+        m = args.e2e_steps
+
+        def e2e_call():
+            mo, sfa = uq.run_mc(plan, grid, cfg, burgers_sines,
+                                [uq.FieldMoments(grid, 1), uq.StructureFunctionAccumulator(2.0, 8)],
+                                workers=args.workers, arith=args.arith, max_steps=m)
+            return float(mo.acc.mean.sum() + mo.acc.m2.sum() + np.sum(sfa.sums))  # D2H of the statistics
+
+        e2e_call()
+        env.barrier()
+        tic = time.perf_counter()
+        for _ in range(args.e2e_reps):
+            e2e_call()
+        torch.cuda.synchronize()
+        el = env.max_over_ranks(time.perf_counter() - tic)
+        e2e = {"value": round(env.ws * cells * 3 * m * args.e2e_reps / el / 1e9, 4), "unit": UNIT,
+               "h2d_bytes_per_step": int(ninst * init.data.nbytes), "d2h_bytes_per_step": int(2 * n * n * 8 + 9 * 8),
+               "step": f"one run_mc call ({ninst} QMC samples, host numpy initial data, max_steps={m}) with "
+                       "moments + structure functions read back",
+               "calls": args.e2e_reps}
     if not burgers:
         from paper_1912_07645_b200.solver import pinned_field
 
@@ -511,6 +546,8 @@ def bench_kh3d(args, env):
     roof = _roofline(8 * 5 * 8 / 3, ws * cells * 3 * args.steps, t_ms * 1e-3,
                      ("ring3i_kernel" if args.arith == "fast" else "ring3_kernel")
                      + "<EULER,HLLC,WENO2> (3+ launches/step)")
+    if args.arith == "fast":
+        _traffic_key(roof, "traffic_kh3d.json")
     roof["achieved"] = round(roof["achieved"] / ws, 1)  # per GPU (the peak is one GPU's)
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
     roof["per"] = "GPU"
