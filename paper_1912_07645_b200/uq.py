@@ -519,6 +519,22 @@ def _ensemble(plan, level, grid, cfg, evaluate_init, slots, lo, hi, batch=None, 
     from .initdev import DeviceInit
 
     on_device = isinstance(evaluate_init, DeviceInit)  # initial data evaluated on the GPU: no host side at all
+    try:
+        _run_batches(plan, level, grid, cfg, evaluate_init, slots, batches, prepare, on_device, ctx, layout, desc,
+                     ncomp, where, arith, max_steps)
+    finally:
+        if evals:
+            evals.shutdown(cancel_futures=True)
+
+
+def _run_batches(plan, level, grid, cfg, evaluate_init, slots, batches, prepare, on_device, ctx, layout, desc,
+                 ncomp, where, arith, max_steps):
+    """_ensemble's batch loop: batch b+1's host initial data is prepared on a
+    helper thread while batch b runs."""
+    import concurrent.futures as cf
+
+    import torch
+
     like = None
     with cf.ThreadPoolExecutor(max_workers=1) as pool:
         nxt = pool.submit(prepare, batches[0], 0) if batches and not on_device else None
@@ -559,8 +575,6 @@ def _ensemble(plan, level, grid, cfg, evaluate_init, slots, lo, hi, batch=None, 
                     continue
                 for i in range(len(ks)):
                     s.push(ctx, desc, layout, bufs[where_[i]], i, grid, ncomp, like)
-    if evals:
-        evals.shutdown()
 
 
 @dataclass
