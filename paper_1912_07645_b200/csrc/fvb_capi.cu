@@ -290,6 +290,7 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
     if (const char* e = getenv("FVB_BLOCKS_PER_SM")) per_sm = std::max(1, atoi(e));
     if (const char* e = getenv("FVB_WAVES")) waves = std::max(1, atoi(e));
     const int64_t slots = (int64_t)sm_count() * per_sm;
+    if (getenv("FVB_DEBUG_GRID")) fprintf(stderr, "fvb stage grid: %lld resident blocks per SM\n", (long long)per_sm);
     const int64_t base = strips * ytiles * nig;
     int64_t want_chunks = 1;
     if (getenv("FVB_WAVES")) {
@@ -328,6 +329,9 @@ static dim3 stage_grid(const fvb_scheme& s, StageParams& p, int ninst, int64_t r
   }
   p.H = (int)H;
   p.chunks = (int)chunks;
+  if (getenv("FVB_DEBUG_GRID"))
+    fprintf(stderr, "fvb stage grid: dim %d variant %d grid (%u,%u,%u) H %lld chunks %lld sms %d\n", s.dim, p.variant,
+            g.x, g.y, g.z, (long long)H, (long long)chunks, sm_count());
   p.nblocks = (unsigned)(g.x * g.y * (s.dim == 3 ? chunks : 1) * (s.dim == 2 ? chunks : 1));
   if (s.dim == 2) p.nblocks = (unsigned)(g.x * chunks);
   if (s.dim == 3) p.nblocks = (unsigned)(g.x * g.y * chunks);
