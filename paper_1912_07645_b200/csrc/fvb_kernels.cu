@@ -224,6 +224,27 @@ int launch_stage_d1(int eq, int flux, int recon, const StageParams& p, dim3 grid
 int launch_stage_d2(int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s) {
   return launch_dim<2>(eq, flux, recon, p, grid, s);
 }
+#if FVB_BLOCK_TIMES && FVB_FAST
+}  // namespace FVB_NS
+}  // namespace fvb
+// diagnostic (variant builds only): per-block [start, end] ns and SM of the
+// last pair-kernel launch of each RK stage; out: 3 x 8192 x 3 uint64
+extern "C" int fvb_debug_block_times(unsigned long long* out) {
+  static unsigned long long t[3][8192][2];
+  static unsigned sm[3][8192];
+  if (cudaMemcpyFromSymbol(t, fvb::fast::g_bt, sizeof(t)) != cudaSuccess) return 6;
+  if (cudaMemcpyFromSymbol(sm, fvb::fast::g_bt_sm, sizeof(sm)) != cudaSuccess) return 6;
+  for (int k = 0; k < 3; ++k)
+    for (int b = 0; b < 8192; ++b) {
+      out[(k * 8192 + b) * 3 + 0] = t[k][b][0];
+      out[(k * 8192 + b) * 3 + 1] = t[k][b][1];
+      out[(k * 8192 + b) * 3 + 2] = sm[k][b];
+    }
+  return 0;
+}
+namespace fvb {
+namespace FVB_NS {
+#endif
 #elif FVB_KDIM == 3
 int launch_stage_d3(int eq, int flux, int recon, const StageParams& p, dim3 grid, cudaStream_t s) {
   return launch_dim<3>(eq, flux, recon, p, grid, s);

@@ -1234,6 +1234,18 @@ __device__ __forceinline__ void cp_async16(double* dst, const double* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
 }
 
+#ifndef FVB_BLOCK_TIMES
+#define FVB_BLOCK_TIMES 0  // 1: record per-block start/end (globaltimer) and SM of the last pair-kernel launch per stage
+#endif
+#if FVB_BLOCK_TIMES
+__device__ unsigned long long g_bt[3][8192][2];
+__device__ unsigned g_bt_sm[3][8192];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 constexpr int kPairNT = 32;                // one warp
 constexpr int kPairW = 2 * kPairNT + 2;    // ring row width: cells x0-2 .. x0+63
 
@@ -1259,6 +1271,9 @@ pair_kernel(const StageParams p) {
 
 #if FVB_PDL
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#endif
+#if FVB_BLOCK_TIMES
+  const unsigned long long bt0 = gtimer();
 #endif
   const int inst = blockIdx.z;
   FvbState* st = p.st + (p.shared_state ? 0 : inst);
@@ -1503,6 +1518,18 @@ pair_kernel(const StageParams p) {
         atomicMin(&st->stage_err, ((long long)p.stage_idx << 42) | ((long long)(1 + a) << 40));
   }
   if constexpr (FIN) block_epilogue<DIM>(p, st, inst, smax, true);
+#if FVB_BLOCK_TIMES
+  if (threadIdx.x == 0 && p.stage_idx < 3) {
+    const unsigned b = blockIdx.y * gridDim.x + blockIdx.x;
+    if (b < 8192) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      g_bt[p.stage_idx][b][0] = bt0;
+      g_bt[p.stage_idx][b][1] = gtimer();
+      g_bt_sm[p.stage_idx][b] = sm;
+    }
+  }
+#endif
 }
 
 template <int EQ>
