@@ -47,6 +47,7 @@ def main(out_path):
     assert lib.fvb_debug_block_times(buf) == 0
     a = np.frombuffer(buf, dtype=np.uint64).reshape(3, 8192, 3).astype(np.int64)
     run.end()
+    np.save(str(Path(out_path).with_suffix(".npy")), a)  # raw [stage][block][t0, t1, sm]
     res = {}
     for k in range(3):
         rows = a[k]

@@ -26,6 +26,11 @@ def algorithmic(cap, name):
     if cap in ("kh2d", "kh2d_pair"):   # KH2D 1024^2, 4 comps: r u^s + w out (+ r u^n)
         stage = 2 if (", 1, 0" in name and "pair" in name) or ", 64, 1, 0" in name else 3
         return 1024 * 1024 * 4 * 8 * stage, f"1024^2 cells x 4 comps x 8 B x {stage} (r u^s, w out{', r u^n' if stage == 3 else ''})"
+    if cap == "mc_pair" and "pair_kernel" in name:   # batched MC: 16 KH2D instances x 512^2
+        stage = 2 if "0, 1, 1, 1, 0>" in name else 3
+        return 16 * 512 * 512 * 4 * 8 * stage, f"16 x 512^2 cells x 4 comps x 8 B x {stage}"
+    if cap == "mc_pair" and "init_eval" in name:
+        return 16 * 512 * 512 * 4 * 8, "16 samples x 512^2 cells x 4 comps x 8 B written"
     if cap == "bqmc_pair":             # 4 Burgers instances x 2048^2, pair kernel (fast default)
         stage = 2 if "1, 0, 1, 1, 0>" in name else 3
         return 4 * 2048 * 2048 * 8 * stage, f"4 x 2048^2 cells x 8 B x {stage}"
