@@ -1311,22 +1311,17 @@ pair_kernel(const StageParams p) {
     if (vec_all) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) cp_async16(&RG(slot, c, 2 * t), us + (pa + ro + c * cs));
-      if (t == 0) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) cp_async16(&RG(slot, c, 64), us + (qa + ro + c * cs));
-      }
+      // pair 32 (cells x0+62, x0+63): one component per lane, in parallel
+      if (t < NC) cp_async16(&RG(slot, t, 64), us + (qa + ro + t * cs));
     } else {
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         cp_async8(&RG(slot, c, 2 * t), us + (pa + ro + c * cs));
         cp_async8(&RG(slot, c, 2 * t + 1), us + (pb + ro + c * cs));
       }
-      if (t == 0) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          cp_async8(&RG(slot, c, 64), us + (qa + ro + c * cs));
-          cp_async8(&RG(slot, c, 65), us + (qb + ro + c * cs));
-        }
+      if (t < NC) {
+        cp_async8(&RG(slot, t, 64), us + (qa + ro + t * cs));
+        cp_async8(&RG(slot, t, 65), us + (qb + ro + t * cs));
       }
     }
   };
