@@ -113,6 +113,28 @@ def test_run_mlmc_matches_reference(P, golden, name):
     assert O.sha16(res.variance) == case["var_sha"]
 
 
+@pytest.mark.parametrize("name", ["kh2d_mlmc_2lvl", "kh2d_mlmc_qmc_2lvl"])
+def test_run_mlmc_fast_within_tolerance(P, golden, name):
+    """run_mlmc in fast arithmetic (the fast-mode default kernels on every
+    level) against the exact run, which test_run_mlmc_matches_reference pins
+    bitwise to the reference: mean and second moment within relative L1
+    1e-12, the variance (a difference of moments) within 1e-10."""
+    from paper_1912_07645_b200 import uq
+    from paper_1912_07645_b200.initial import kelvin_helmholtz
+
+    case = next(u for u in golden["mlmc"] if u["name"] == name)
+    _, cfg = product_objects(case["scheme"])
+    grids = tuple(P.GridSpec(2, tuple(c), (0.0, 0.0), (1.0, 1.0), ghost_width=2) for c in case["cells"])
+    plan = uq.MlmcPlan(grids, tuple(case["samples"]), method=case["method"], seed=case["seed"],
+                       stochastic_dim=case["stochastic_dim"])
+    ref = uq.run_mlmc(plan, lambda g: cfg, kelvin_helmholtz, arith="exact")
+    assert O.sha16(ref.mean) == case["mean_sha"]
+    got = uq.run_mlmc(plan, lambda g: cfg, kelvin_helmholtz, arith="fast")
+    assert rel_l1(got.mean, ref.mean) <= 1e-12
+    assert rel_l1(got.second_moment, ref.second_moment) <= 1e-12
+    assert rel_l1(got.variance, ref.variance) <= 1e-10
+
+
 def test_histogram_functional_matches_reference(P, golden):
     from paper_1912_07645_b200 import uq
     from paper_1912_07645_b200.initial import kelvin_helmholtz
