@@ -112,6 +112,23 @@ _SIGS = {
 EXPORTS = tuple(_SIGS)
 
 
+def _warn_if_stale(lib_path: Path) -> None:
+    """The in-tree library records the digest of the sources it was built
+    from (build.py); loading one built from other sources (e.g. a tuning
+    variant left behind) would silently measure the wrong code."""
+    try:
+        from . import build as B
+
+        stamp = lib_path.parent / "build.sha256"
+        if stamp.exists() and stamp.read_text().split("|")[0] != B._sources_digest():
+            import warnings
+
+            warnings.warn(f"{lib_path} was built from different sources than the ones in csrc/: "
+                          "rebuild with `python -m paper_1912_07645_b200.build`", RuntimeWarning)
+    except Exception:
+        pass
+
+
 def load_library(path: Path | None = None) -> C.CDLL:
     """Load libfvb200.so (no GPU needed); raise NativeUnavailable if absent."""
     global _lib
@@ -123,6 +140,8 @@ def load_library(path: Path | None = None) -> C.CDLL:
             raise NativeUnavailable(
                 f"{p} is missing: build it with `python -m paper_1912_07645_b200.build` "
                 "(there is no CPU fallback for the finite-volume hot path)")
+        if path is None and not os.environ.get("FVB_LIB"):
+            _warn_if_stale(p)
         lib = C.CDLL(str(p))
         for name, (args, res) in _SIGS.items():
             fn = getattr(lib, name)
