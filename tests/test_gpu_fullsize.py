@@ -116,3 +116,98 @@ def test_run_mc_sharded_over_ranks(golden):
     for c in range(4):
         assert rel_l1(out["mean"][c], m1.acc.mean[c]) <= 1e-14
     assert rel_l1(out["m2"], m1.acc.m2) <= 1e-12
+
+
+KH_DEV = ["y < 0.25 + 0.01 * sin(2 * pi * (x + X0)) ? 1.0 : (y < 0.75 + 0.01 * sin(2 * pi * (x + X1)) ? 2.0 : 1.0)",
+          "y < 0.25 + 0.01 * sin(2 * pi * (x + X2)) ? -0.5 : (y < 0.75 + 0.01 * sin(2 * pi * (x + X3)) ? 0.5 : -0.5)"]
+
+
+def test_kh3d_largest_size_fast_vs_exact():
+    """KH3D at 896^3: 5 x 900^3 = 3.6e9 elements per field (component offsets
+    past 2^31, four 29 GB fields resident), initial data evaluated on the
+    device, one RK3 step in exact and in fast arithmetic: the exact kernels
+    are pinned bitwise to the oracle at smaller sizes, so their agreement here
+    checks the fast 3D path (and both kernels' indexing) at the largest size
+    that leaves room for the comparison.  The y/z momenta of the extruded
+    preset are round-off at t = 0: measured against 1e-3 of the largest
+    component's norm (helpers.rel_l1_field)."""
+    import torch
+
+    import paper_1912_07645_b200 as P
+    from paper_1912_07645_b200 import _native as N
+    from paper_1912_07645_b200.initdev import DeviceInit
+    from paper_1912_07645_b200.solver import DeviceRun
+
+    if torch.cuda.get_device_properties(0).total_memory < 150e9:
+        pytest.skip("needs a 180 GB B200")
+    n = 896
+    grid = P.GridSpec(3, (n, n, n), (0.0,) * 3, (1.0,) * 3, ghost_width=2)
+    cfg = P.SchemeConfig(P.EquationModel("euler", 3), P.FluxKind.HLLC,
+                         P.Reconstruction(P.ReconstructionKind.WENO2), rk_order=3, cfl=0.475, t_end=2.0)
+    init = torch.empty((1, 5) + tuple(grid.padded[::-1]), dtype=torch.float64, device="cuda")
+    errs = DeviceInit(KH_DEV + ["0.0", "0.0", "2.5"], cfg.model, primitive=True).evaluate_batch(grid, [KH_VEC], init)
+    assert errs[0] is None
+
+    def one_step(b0, arith):
+        bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
+        run = DeviceRun(grid, cfg, bufs, 1, N.MODE_FIXED, 1, arith, log=False)
+        run.steps(1)
+        infos = run.end()
+        assert infos[0].err == 0 and infos[0].steps == 1
+        del bufs[1:]
+        return b0, infos[0].dt
+
+    ex, dt_ex = one_step(init.clone(), "exact")
+    fa, dt_fa = one_step(init, "fast")
+    assert abs(dt_fa - dt_ex) <= 1e-12 * dt_ex
+    g = grid.ghost_width
+    sl = (0, slice(None)) + tuple(slice(g, g + m) for m in grid.interior_shape)
+    a, b = fa[sl], ex[sl]
+    norms = [float(b[c].abs().sum()) for c in range(5)]
+    errs = [float((a[c] - b[c]).abs().sum()) for c in range(5)]
+    big = max(norms)
+    worst = max(e / max(nm, 1e-3 * big) for e, nm in zip(errs, norms))
+    assert worst <= 1e-12, (worst, errs, norms)
+
+
+def test_kh2d_largest_size_fast_vs_exact():
+    """KH2D at 16384^2 (4 x 16388^2 = 1.07e9 elements per field, near the 2^31
+    32-bit offset span the 2D kernels accept): one RK3 step in exact and fast
+    arithmetic from device-evaluated initial data, fields within relative L1
+    1e-12 (the exact kernels are pinned bitwise to the oracle at smaller
+    sizes)."""
+    import torch
+
+    import paper_1912_07645_b200 as P
+    from paper_1912_07645_b200 import _native as N
+    from paper_1912_07645_b200.initdev import DeviceInit
+    from paper_1912_07645_b200.solver import DeviceRun
+
+    n = 16384
+    grid = P.GridSpec(2, (n, n), (0.0, 0.0), (1.0, 1.0), ghost_width=2)
+    cfg = P.SchemeConfig(P.EquationModel("euler", 2), P.FluxKind.HLLC,
+                         P.Reconstruction(P.ReconstructionKind.WENO2), rk_order=3, cfl=0.475, t_end=2.0)
+    init = torch.empty((1, 4) + tuple(grid.padded[::-1]), dtype=torch.float64, device="cuda")
+    errs = DeviceInit(KH_DEV + ["0.0", "2.5"], cfg.model, primitive=True).evaluate_batch(grid, [KH_VEC], init)
+    assert errs[0] is None
+
+    def one_step(b0, arith):
+        bufs = [b0, torch.empty_like(b0), torch.empty_like(b0)]
+        run = DeviceRun(grid, cfg, bufs, 1, N.MODE_FIXED, 1, arith, log=False)
+        run.steps(1)
+        infos = run.end()
+        assert infos[0].err == 0 and infos[0].steps == 1
+        del bufs[1:]
+        return b0, infos[0].dt
+
+    ex, dt_ex = one_step(init.clone(), "exact")
+    fa, dt_fa = one_step(init, "fast")
+    assert abs(dt_fa - dt_ex) <= 1e-12 * dt_ex
+    g = grid.ghost_width
+    sl = (0, slice(None), slice(g, g + n), slice(g, g + n))
+    a, b = fa[sl], ex[sl]
+    norms = [float(b[c].abs().sum()) for c in range(4)]
+    errs = [float((a[c] - b[c]).abs().sum()) for c in range(4)]
+    big = max(norms)
+    worst = max(e / max(nm, 1e-3 * big) for e, nm in zip(errs, norms))
+    assert worst <= 1e-12, (worst, errs, norms)
